@@ -1,0 +1,227 @@
+/*
+ * bht_b200.h — C ABI of the B200-native bulk hash-table hot path.
+ *
+ * This is the drop-in boundary for the reference library's table API
+ * (reference: proj/include/bht/table.hpp, proj/include/bht/core.hpp).  Every
+ * entry point below names the reference interface it replaces.  Signatures
+ * carry only plain pointers, sizes and PODs; `stream` is a `cudaStream_t`
+ * passed as `void*` (NULL = the legacy default stream).
+ *
+ * The implementation lives in paper_2108_07232_b200/csrc and is built into
+ * paper_2108_07232_b200/lib/libbht_b200.so.  There is no CPU fallback: every
+ * compute entry point runs hand-written sm_100a kernels and returns
+ * BHT_CUDA_ERROR if no device is usable.
+ *
+ * Conventions kept bit-exact with the reference:
+ *   - slot = (value << 32) | key, empty slot = all ones      (core.hpp:13-41)
+ *   - user keys live in [0, 2^32-2]; 0xFFFFFFFF is the sentinel (core.hpp:20-24)
+ *   - h_i(k) = ((alpha_i*k + beta_i) mod 4294967291) mod range_i (hash.hpp:21-23)
+ *   - kind order one_cht, bcht, bp2ht, iht                   (core.hpp:43)
+ *   - store layout: bucket-major, b consecutive 8-byte slots  (table.hpp:42-47)
+ *
+ * Error model (reference: exceptions in core.cpp:40-60, table.cpp:15-17,22-23,225):
+ * nothing throws; a bht_status is returned and bht_last_error_string() holds
+ * the message.  A failed insertion (cuckoo chain cap, all candidate buckets
+ * full) is NOT an error: status stays BHT_OK and the failure is reported in
+ * bht_insert_result, as `build_outcome` does in the reference (table.hpp:115-120).
+ */
+#ifndef BHT_B200_H_
+#define BHT_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BHT_EMPTY_KEY 0xFFFFFFFFu            /* core.hpp:20 */
+#define BHT_EMPTY_VALUE 0xFFFFFFFFu          /* core.hpp:21 */
+#define BHT_EMPTY_SLOT 0xFFFFFFFFFFFFFFFFull /* core.hpp:22 */
+#define BHT_HASH_PRIME 4294967291ull         /* hash.hpp:12 */
+#define BHT_MAX_HASHES 4
+#define BHT_MAX_BUCKET_SIZE 64               /* core.hpp:79 */
+
+typedef enum bht_status {
+  BHT_OK = 0,
+  BHT_INVALID_ARGUMENT = 1,  /* std::invalid_argument in the reference */
+  BHT_KIND_MISMATCH = 2,     /* std::logic_error (table.cpp:15-17) */
+  BHT_CAPACITY_EXCEEDED = 3, /* "build: key set exceeds table capacity" (table.cpp:225) */
+  BHT_CUDA_ERROR = 4,
+  BHT_COMM_ERROR = 5,
+  BHT_IO_ERROR = 6           /* std::runtime_error on file I/O (table.cpp:43,50) */
+} bht_status;
+
+/* table_kind, same numeric order as the reference enum (core.hpp:43). */
+typedef enum bht_kind {
+  BHT_ONE_CHT = 0, /* b = 1, 4 hash functions */
+  BHT_BCHT = 1,    /* 3 hash functions */
+  BHT_BP2HT = 2,   /* 2 hash functions */
+  BHT_IHT = 3      /* primary + 2 secondaries */
+} bht_kind;
+
+/* Plain-data image of the reference `table_config` (core.hpp:66-77).  The
+ * per-hash (alpha, beta, range) triples are `hash_params` (hash.hpp:11-19). */
+typedef struct bht_config {
+  int32_t kind;         /* bht_kind */
+  uint32_t bucket_size; /* b: power of two in [1, 64] */
+  uint64_t num_buckets; /* m */
+  uint64_t capacity;    /* m * b */
+  uint32_t n_hashes;    /* hash_count(kind): 4 / 3 / 2 / 3 (core.hpp:49-57) */
+  uint32_t threshold;   /* t, iht only */
+  uint32_t max_chain;   /* cuckoo kinds only */
+  uint32_t reserved;
+  uint64_t seed;
+  uint64_t alpha[BHT_MAX_HASHES];
+  uint64_t beta[BHT_MAX_HASHES];
+  uint64_t range[BHT_MAX_HASHES];
+} bht_config;
+
+/* Image of `build_outcome` (table.hpp:115-120) for one bulk insert call. */
+typedef struct bht_insert_result {
+  uint64_t attempted;        /* n of this call */
+  uint64_t inserted;         /* pairs now resident because of this call */
+  uint64_t failed;           /* pairs dropped (chain cap / all candidates full) */
+  uint64_t probes;           /* bucket reads, probe_stats.total_probes (probe_stats.hpp:12-31) */
+  uint32_t first_failed_key; /* some dropped key, BHT_EMPTY_KEY if none */
+  uint32_t success;          /* inserted == attempted */
+} bht_insert_result;
+
+typedef struct bht_find_result {
+  uint64_t queries;
+  uint64_t hits;         /* queries answered with a value */
+  uint64_t probes;       /* bucket reads */
+  uint64_t value_sum;    /* sum of the returned values of the hits (checksum) */
+} bht_find_result;
+
+/* Where the caller's key / value / output arrays live. */
+typedef enum bht_mem_space {
+  BHT_MEM_DEVICE = 0, /* device pointers on the table's device */
+  BHT_MEM_HOST = 1    /* host pointers (pinned or pageable); the call stages chunks over PCIe */
+} bht_mem_space;
+
+typedef struct bht_table bht_table; /* opaque: replaces `class hash_table` (table.hpp:28-80) */
+
+/* ---- configuration (host only, no GPU needed) ------------------------------------------- */
+
+/* Replaces make_config (core.hpp:85-91, core.cpp:33-68) bit-exactly: same ceil(n/(lf*b)),
+ * same default threshold b*80/100 and max(7*ceil(log2 n),128) chain cap, same hash-constant
+ * draw from xorshift_rng(mix_seed(seed, 0x68617368)).  threshold < 0 / max_chain < 0 select
+ * the defaults (std::nullopt in the reference). */
+bht_status bht_make_config(int32_t kind, uint64_t n_keys, double load_factor, uint32_t bucket_size,
+                           int64_t threshold, uint64_t seed, int64_t max_chain, bht_config* out);
+
+/* hash_count (core.hpp:49-57); 0 for an unknown kind. */
+uint32_t bht_hash_count(int32_t kind);
+/* default_max_chain (core.cpp:28-31). */
+uint32_t bht_default_max_chain(uint64_t n_keys);
+/* mix_seed (hash.hpp:33-35), exposed so harnesses derive the same seed streams. */
+uint64_t bht_mix_seed(uint64_t seed, uint64_t stream);
+/* bucket_index (hash.hpp:21-23) evaluated on the host with the SAME division-free arithmetic
+ * the device hash stage uses (fold by 2^32 = 5 mod p, then a 64-bit reciprocal for mod range). */
+uint64_t bht_bucket_index_host(uint64_t alpha, uint64_t beta, uint64_t range, uint32_t key);
+/* value_for_key (keygen.hpp:23-26). */
+uint32_t bht_value_for_key(uint32_t key);
+/* predict_sectors (sector_model.hpp:26-31); op: 0 = insert, 1 = find. */
+double bht_predict_sectors(int32_t kind, uint32_t bucket_size, double mean_probes, int32_t op);
+
+/* ---- lifetime ---------------------------------------------------------------------------- */
+
+/* Replaces hash_table::hash_table(table_config) (table.cpp:21-32): allocates the m*b slot store
+ * in device memory (256-byte aligned) on `device` and fills it with BHT_EMPTY_SLOT.
+ * BHT_INVALID_ARGUMENT on a wrong hash count (table.cpp:22-23) or an inconsistent config. */
+bht_status bht_create(const bht_config* cfg, int32_t device, bht_table** out);
+bht_status bht_destroy(bht_table* table);
+/* Re-initialises the store to empty and zeroes the inserted counter (a fresh hash_table). */
+bht_status bht_clear(bht_table* table, void* stream);
+bht_status bht_get_config(const bht_table* table, bht_config* out);
+int32_t bht_device_of(const bht_table* table);
+
+/* ---- the hot path ------------------------------------------------------------------------ */
+
+/* Bulk insert: replaces build()'s insertion loop (table.cpp:224-271) and insert_pair
+ * (table.cpp:203-212) with explicit values.  Precondition as in the reference: keys unique,
+ * != sentinel, not yet present.  Unlike the reference's build, which stops at the first failed
+ * key, every pair is attempted.  BHT_CAPACITY_EXCEEDED when inserted + n > capacity.
+ * `result` may be NULL (no synchronisation; fetch it later with bht_last_insert_result). */
+bht_status bht_insert(bht_table* table, const uint32_t* keys, const uint32_t* values, uint64_t n,
+                      int32_t mem_space, bht_insert_result* result, void* stream);
+
+/* Bulk find: replaces the caller-side `for q: find_key(table, q.key, stats)` loop
+ * (experiments.cpp:92, oracle.cpp:21-27) and find_key (table.cpp:214-222).
+ * out_values[i] = value, or BHT_EMPTY_VALUE when the key is absent. */
+bht_status bht_find(const bht_table* table, const uint32_t* keys, uint32_t* out_values, uint64_t n,
+                    int32_t mem_space, bht_find_result* result, void* stream);
+
+/* bcht/1cht find without the early exit: bcht_find_no_early_exit (oracle.cpp:56-63). */
+bht_status bht_find_exhaustive(const bht_table* table, const uint32_t* keys, uint32_t* out_values,
+                               uint64_t n, int32_t mem_space, bht_find_result* result, void* stream);
+
+/* Synchronises `stream` and returns the counters of the most recent insert / find. */
+bht_status bht_last_insert_result(bht_table* table, bht_insert_result* out, void* stream);
+/* Keys dropped by inserts since the last bht_clear (at most `max_keys` copied). */
+bht_status bht_failed_keys(bht_table* table, uint32_t* host_out, uint64_t max_keys, uint64_t* count);
+/* iht only: select the prose variant of iht_insert (table.cpp:167-169, `prose_fallback`). */
+bht_status bht_set_iht_prose_fallback(bht_table* table, int32_t enabled);
+
+/* ---- load factor / store access ---------------------------------------------------------- */
+
+/* realized_load() (table.hpp:40): inserted counter and capacity. */
+bht_status bht_load_factor(const bht_table* table, uint64_t* inserted, uint64_t* capacity);
+/* occupied_slots() (table.cpp:34-39): streaming count of non-empty keys in the store. */
+bht_status bht_count_occupied(const bht_table* table, uint64_t* occupied, void* stream);
+/* slot_at over the whole store (table.hpp:53): copies m*b slots to host, bucket order. */
+bht_status bht_download_store(const bht_table* table, uint64_t* host_dst, void* stream);
+/* poke_slot over the whole store (table.hpp:54-56): replaces the store; recounts `inserted`. */
+bht_status bht_upload_store(bht_table* table, const uint64_t* host_src, void* stream);
+/* dump_store (table.cpp:41-51): little-endian u64 per slot, bucket order. */
+bht_status bht_dump_store(const bht_table* table, const char* path);
+/* check_admissibility (oracle.cpp:40-54) evaluated on the device: pairs outside every bucket
+ * their hash functions name. */
+bht_status bht_count_inadmissible(const bht_table* table, uint64_t* violations, void* stream);
+/* Raw device pointer of the store (for zero-copy interop); valid until bht_destroy. */
+uint64_t* bht_device_store(const bht_table* table);
+
+/* ---- hash stage in isolation (parity hook for hash.hpp:21-23) ---------------------------- */
+
+/* out[i] = bucket_index({alpha, beta, range}, keys[i]) computed by the device hash stage. */
+bht_status bht_hash_keys(uint64_t alpha, uint64_t beta, uint64_t range, const uint32_t* keys,
+                         uint32_t* out, uint64_t n, int32_t mem_space, int32_t device, void* stream);
+
+/* ---- sharded table: key-range partitioning for multi-GPU (no reference counterpart) ------ */
+
+/* owner(k) = (g(k) * n_shards) >> 32 with g(k) = (alpha*k + beta) mod p scaled to 32 bits. */
+uint32_t bht_shard_of_host(uint64_t alpha, uint64_t beta, uint32_t n_shards, uint32_t key);
+
+/* Partition n keys (and optional values) by owner shard.  Writes keys (values) grouped by shard
+ * into out_keys (out_values), the original position of every routed element into out_index
+ * (may be NULL), and the per-shard counts into counts_host[n_shards] (host memory; the call
+ * synchronises `stream`).  All array pointers are device pointers on `device`. */
+bht_status bht_shard_partition(uint64_t alpha, uint64_t beta, uint32_t n_shards,
+                               const uint32_t* keys, const uint32_t* values, uint64_t n,
+                               uint32_t* out_keys, uint32_t* out_values, uint32_t* out_index,
+                               uint64_t* counts_host, int32_t device, void* stream);
+
+/* out[index[i]] = answers[i]: puts routed answers back into the caller's query order. */
+bht_status bht_shard_unpermute(const uint32_t* answers, const uint32_t* index, uint64_t n,
+                               uint32_t* out, int32_t device, void* stream);
+
+/* ---- synthetic workload (keygen.cpp:50-64 protocol on the device) ------------------------ */
+
+/* keys[i] = a bijection of (offset + i) over [0, 2^32-2]: unique, sentinel-free keys without a
+ * host-side rejection set.  Indices >= some n are guaranteed-absent negatives. */
+bht_status bht_generate_unique_keys(uint64_t seed, uint64_t offset, uint64_t n, uint32_t* out_keys,
+                                    uint32_t* out_values, int32_t device, void* stream);
+
+/* ---- diagnostics ------------------------------------------------------------------------- */
+
+const char* bht_last_error_string(void);
+const char* bht_version_string(void);
+/* Number of kernels this library has launched in this process (bench.py's gpu_launches). */
+uint64_t bht_kernel_launch_count(void);
+size_t bht_sizeof_config(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BHT_B200_H_ */
