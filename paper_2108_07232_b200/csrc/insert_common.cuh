@@ -1,0 +1,42 @@
+// insert_common.cuh — pieces shared by the three bulk-insert kernels.
+#pragma once
+#include "kernels.h"
+
+namespace bht_b200 {
+
+constexpr int kInsertBlock = 256;
+
+// Appends a dropped key to the table's failed-key log (the GPU image of build_outcome::failed_key,
+// reference: proj/include/bht/table.hpp:115-120; a bulk insert can drop more than one).
+__device__ __forceinline__ void record_failed(DevCounters* ctr, uint32_t* failed_keys, uint64_t failed_cap, uint32_t key) {
+  const unsigned long long pos = atomicAdd(&ctr->failed_recorded, 1ull);
+  if (pos < failed_cap) failed_keys[pos] = key;
+  atomicMin(&ctr->first_failed_key, key);
+}
+
+__device__ __forceinline__ void flush_insert_counters(DevCounters* ctr, int lane, uint32_t n_ins, uint32_t n_fail,
+                                                      uint32_t n_probe) {
+  const unsigned long long a = warp_sum(n_ins), f = warp_sum(n_fail), p = warp_sum(n_probe);
+  if (lane == 0) {
+    if (a) {
+      atomicAdd(&ctr->inserted, a);
+      atomicAdd(&ctr->inserted_total, a);
+    }
+    if (f) atomicAdd(&ctr->failed, f);
+    if (p) atomicAdd(&ctr->insert_probes, p);
+  }
+}
+
+#define BHT_DISPATCH_BUCKET_SIZE(b, CALL)  \
+  switch (b) {                             \
+    case 1: return CALL(1);                \
+    case 2: return CALL(2);                \
+    case 4: return CALL(4);                \
+    case 8: return CALL(8);                \
+    case 16: return CALL(16);              \
+    case 32: return CALL(32);              \
+    case 64: return CALL(64);              \
+    default: return cudaErrorInvalidValue; \
+  }
+
+}  // namespace bht_b200

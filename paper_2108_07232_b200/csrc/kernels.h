@@ -1,0 +1,64 @@
+// kernels.h — host-side launch interface between the C ABI (capi.cu) and the kernel TUs.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "probe_engine.cuh"
+
+namespace bht_b200 {
+
+struct LaunchGeom {
+  int sm_count;
+};
+
+// find.cu — K3 bulk_find<kind, b>.  early_exit selects bcht_find's non-full early exit
+// (table.cpp:104); without it the same kernel is bp2ht_find / iht_find / bcht_find_no_early_exit.
+cudaError_t launch_find(const TableView& t, bool early_exit, const uint32_t* keys, uint32_t* out, uint64_t n,
+                        DevCounters* ctr, int sm_count, cudaStream_t stream);
+
+// insert_cuckoo.cu — K4 (bcht, 1cht); insert_p2.cu — K5 (bp2ht); insert_iht.cu — K6 (iht).
+cudaError_t launch_insert_cuckoo(const TableView& t, const uint32_t* keys, const uint32_t* values, uint64_t n,
+                                 DevCounters* ctr, uint32_t* failed_keys, uint64_t failed_cap, int sm_count,
+                                 cudaStream_t stream);
+cudaError_t launch_insert_p2(const TableView& t, const uint32_t* keys, const uint32_t* values, uint64_t n,
+                             DevCounters* ctr, uint32_t* failed_keys, uint64_t failed_cap, int sm_count,
+                             cudaStream_t stream);
+cudaError_t launch_insert_iht(const TableView& t, const uint32_t* keys, const uint32_t* values, uint64_t n,
+                              DevCounters* ctr, uint32_t* failed_keys, uint64_t failed_cap, int sm_count,
+                              cudaStream_t stream);
+
+// util.cu — K0 fill, K7 count, admissibility, hash hook, K8/K9 shard routing, synthetic keys.
+cudaError_t launch_fill_empty(uint64_t* store, uint64_t n_slots, int sm_count, cudaStream_t stream);
+cudaError_t launch_count_occupied(const uint64_t* store, uint64_t n_slots, unsigned long long* out, int sm_count,
+                                  cudaStream_t stream);
+cudaError_t launch_count_inadmissible(const TableView& t, unsigned long long* out, int sm_count, cudaStream_t stream);
+cudaError_t launch_hash_keys(const HashFn& h, const uint32_t* keys, uint32_t* out, uint64_t n, int sm_count,
+                             cudaStream_t stream);
+constexpr int kMaxShards = 256;
+cudaError_t launch_shard_histogram(uint32_t alpha, uint32_t beta, uint32_t n_shards, const uint32_t* keys, uint64_t n,
+                                   unsigned long long* counts, int sm_count, cudaStream_t stream);
+cudaError_t launch_shard_scatter(uint32_t alpha, uint32_t beta, uint32_t n_shards, const uint32_t* keys,
+                                 const uint32_t* values, uint64_t n, unsigned long long* cursors, uint32_t* out_keys,
+                                 uint32_t* out_values, uint32_t* out_index, int sm_count, cudaStream_t stream);
+cudaError_t launch_unpermute(const uint32_t* answers, const uint32_t* index, uint64_t n, uint32_t* out, int sm_count,
+                             cudaStream_t stream);
+cudaError_t launch_generate_keys(uint64_t seed, uint64_t offset, uint64_t n, uint32_t* keys, uint32_t* values,
+                                 int sm_count, cudaStream_t stream);
+
+// Bumped by every launch_* above (bht_kernel_launch_count).
+void note_launch();
+uint64_t launch_count();
+
+// Persistent grid: enough CTAs of `block` threads to fill the device, never more than the work.
+template <typename Kernel>
+inline int persistent_grid(Kernel kernel, int block, int sm_count, uint64_t work_items, uint64_t items_per_block) {
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, 0) != cudaSuccess || per_sm < 1) per_sm = 1;
+  uint64_t need = (work_items + items_per_block - 1) / items_per_block;
+  if (need < 1) need = 1;
+  const uint64_t fill = static_cast<uint64_t>(per_sm) * static_cast<uint64_t>(sm_count);
+  return static_cast<int>(need < fill ? need : fill);
+}
+
+}  // namespace bht_b200
