@@ -1,0 +1,428 @@
+#!/usr/bin/env python
+"""bench.py — BASELINE.json's metric on B200: bulk insert & bulk find MKeys/s.
+
+A step is one pass of the hot path over one batch: bulk BUILD (clear the store + insert n pairs) followed by
+bulk FIND of n queries (100 % positive), on the configuration the metric is quoted on: BCHT b=16, 50 M
+unique uniformly distributed 32-bit keys (MT19937), load factor 0.9.  `value` = 2n keys / step time with the
+inputs resident in HBM; `e2e` = the same pass through the C ABI with HOST (pinned) buffers, PCIe copies inside
+the timed region.  The other positive fractions (50 %, 0 %) and the per-kernel times are reported in `detail`.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W]            the CUDA path
+    python bench.py --impl reference ...                            the reference CPU implementation (oracle/_ref)
+
+N > 1 (torchrun, one rank per GPU): the sharded table — 50 M keys per GPU generated on the device, NCCL
+all-to-all routing inside the timed region, weak scaling.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+KIND, B, LF, N_KEYS, SEED = "bcht", 16, 0.9, 50_000_000, 1
+METRIC = "insert & find MKeys/s, BCHT b=16, 50M keys, LF 0.9"
+
+
+def make_workload(n: int, seed: int):
+    """n present + n absent unique sentinel-free u32 keys and n values from MT19937 streams (uniform, random order)."""
+    rng = np.random.Generator(np.random.MT19937(seed))
+    raw = rng.integers(0, 0xFFFFFFFF, size=int(2 * n * 1.02) + 1024, dtype=np.uint32)
+    raw.sort()
+    keep = np.empty(raw.size, dtype=bool)
+    keep[0] = True
+    np.not_equal(raw[1:], raw[:-1], out=keep[1:])
+    uniq = raw[keep]
+    assert uniq.size >= 2 * n
+    rng.shuffle(uniq)
+    values = rng.integers(0, 0xFFFFFFFF, size=n, dtype=np.uint32)
+    return uniq[:n].copy(), uniq[n:2 * n].copy(), values
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled DURING the timed region (B200_PROFILING.md recipe)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.path = tempfile.mktemp(suffix=".csv")
+        self.gpu = gpu_index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f,
+                                         stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.f.close()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            p = [x.strip() for x in line.split(",")]
+            if len(p) < 9:
+                continue
+            try:
+                sm.append(float(p[1]))
+                smax = float(p[2])
+            except ValueError:
+                continue
+            for name, v in zip(names, p[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        os.unlink(self.path)
+        # idle samples (before / between launches) sit at low clocks: take the median of the upper half
+        sm.sort()
+        load = sm[len(sm) // 2:] if sm else []
+        return {"sm_mhz": float(np.median(load)) if load else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---- the reference arm: the reference's own CPU implementation -------------------------------------------------
+
+def cpu_reference_pass(ref, cfg, present, queries, n_sample, threads):
+    """One bounded pass of the reference CPU path: build() in parallel mode on all host threads
+    (table.cpp:239-271) + the caller-side find_key loop chunked over the same threads."""
+    table, out = ref.build(present[:n_sample], cfg, parallel=True, workers=threads)
+    t_build = out["seconds"]
+    _, hits, probes, t_find = table.find_bulk_timed(queries[:n_sample], threads)
+    table.close()
+    return t_build, t_find, out, hits
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from oracle import binding
+    ref = binding.ref()
+    threads = ref.hardware_concurrency()
+    n = args.keys
+    present, _absent, _values = make_workload(n, SEED)
+    ocfg = make_ref_config(ref, n)
+    # size the per-step sample so that the whole run ends within a few minutes
+    t0 = time.time()
+    probe_n = min(n, 2_000_000)
+    tb, tf, _, _ = cpu_reference_pass(ref, ocfg, present, present, probe_n, threads)
+    rate = 2 * probe_n / max(tb + tf, 1e-9)
+    budget = 150.0
+    n_sample = int(min(n, max(1_000_000, rate * budget / (args.steps + args.warmup) / 2)))
+    for _ in range(args.warmup):
+        cpu_reference_pass(ref, ocfg, present, present, n_sample, threads)
+    times, tbs, tfs = [], [], []
+    for _ in range(args.steps):
+        tb, tf, out, hits = cpu_reference_pass(ref, ocfg, present, present, n_sample, threads)
+        assert out["success"] and hits == n_sample
+        times.append(tb + tf)
+        tbs.append(tb)
+        tfs.append(tf)
+    total = sum(times)
+    value = 2 * n_sample * args.steps / total / 1e6
+    sample = (f"first {n_sample} of the {n} keys built into the full-size ({ocfg.capacity * 8 / 1e6:.0f} MB) table "
+              f"with the reference's build(parallel, {threads} workers), then {n_sample} positive find_key calls "
+              f"chunked over {threads} threads")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "MKeys/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32/u64 integer",
+        "data": "synthetic: unique uniform u32 keys, MT19937",
+        "config": workload_config(n, args.gpus),
+        "cpu_baseline": {"value": value, "unit": "MKeys/s", "cores": threads, "kind": "reference", "sample": sample,
+                         "insert_mkeys": n_sample * args.steps / sum(tbs) / 1e6,
+                         "find_mkeys": n_sample * args.steps / sum(tfs) / 1e6},
+        "e2e": {"value": value, "unit": "MKeys/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "wall_s": time.time() - t0,
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def make_ref_config(ref, n):
+    from oracle import binding
+    cfg = ref.make_config(binding.KINDS[KIND], n, LF, B, seed=ref.mix_seed(SEED, 0x100))
+    return cfg
+
+
+def workload_config(n, gpus):
+    return {"workload": f"{KIND} b={B}, {n} unique u32 keys/values per GPU, load factor {LF}: bulk build then "
+                        f"{n} positive bulk finds", "kind": KIND, "bucket_size": B, "load_factor": LF,
+            "keys_per_gpu": n, "table_mb": None, "l2": "table and inputs each exceed the 126 MB L2; no flush needed",
+            "parallelism": "single table" if gpus == 1 else f"key-range sharded x{gpus}, NCCL all-to-all"}
+
+
+# ---- the CUDA arm ------------------------------------------------------------------------------------------------
+
+def run_cuda(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2108_07232_b200 as bht
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py: no CUDA device; the CUDA arm has no CPU fallback (use --impl reference)")
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=device)
+    n = args.keys
+    cfg = bht.make_config(KIND, n, LF, B, seed=bht.mix_seed(SEED, 0x100))
+    wl = workload_config(n, world)
+    wl["table_mb"] = cfg.capacity * 8 / 1e6
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    stream = torch.cuda.current_stream()
+    sampler = ClockSampler(local)
+
+    if world == 1:
+        present, absent, values = make_workload(n, SEED)
+        d_keys = torch.from_numpy(present.view(np.int32)).to(device)
+        d_vals = torch.from_numpy(values.view(np.int32)).to(device)
+        d_abs = torch.from_numpy(absent.view(np.int32)).to(device)
+        d_out = torch.empty(n, dtype=torch.int32, device=device)
+        half = n // 2
+        d_mixed = torch.cat([d_keys[:half], d_abs[:n - half]])[torch.randperm(n, device=device)].contiguous()
+        table = bht.HashTable(cfg, local)
+
+        def step(timers=None):
+            e = [ev() for _ in range(4)] if timers is not None else None
+            if e: e[0].record(stream)
+            table.clear()
+            if e: e[1].record(stream)
+            table.insert(d_keys, d_vals, want_result=False)
+            if e: e[2].record(stream)
+            table.find(d_keys, d_out)
+            if e: e[3].record(stream)
+            if timers is not None:
+                timers.append(e)
+
+        for _ in range(max(args.warmup, 3)):
+            step()
+        outcome = table.last_insert_result()
+        assert outcome.success, outcome
+        barrier()
+        launches0 = bht.kernel_launch_count()
+        sampler.start()
+        timers = []
+        t_start, t_end = ev(), ev()
+        t_start.record(stream)
+        for _ in range(args.steps):
+            step(timers)
+        t_end.record(stream)
+        barrier()
+        clocks = sampler.stop()
+        launches = bht.kernel_launch_count() - launches0
+        total_ms = t_start.elapsed_time(t_end)
+        ms_step = total_ms / args.steps
+        clear_ms = float(np.mean([e[0].elapsed_time(e[1]) for e in timers]))
+        ins_ms = float(np.mean([e[1].elapsed_time(e[2]) for e in timers]))
+        find_ms = float(np.mean([e[2].elapsed_time(e[3]) for e in timers]))
+        value = 2 * n / (ms_step * 1e-3) / 1e6
+
+        # probe counts of this very workload (device counters = probe_stats, probe_stats.hpp:12-31)
+        outcome = table.last_insert_result()
+        _, fs100 = table.find(d_keys, d_out, want_stats=True)
+        assert fs100.hits == n
+        checksum_ok = fs100.value_sum == int(values.astype(np.uint64).sum())
+        assert checksum_ok, "find checksum mismatch"
+
+        def timed_find(q):
+            torch.cuda.synchronize()
+            a, b_ = ev(), ev()
+            ts = []
+            for _ in range(3):
+                a.record(stream)
+                table.find(q, d_out)
+                b_.record(stream)
+                torch.cuda.synchronize()
+                ts.append(a.elapsed_time(b_))
+            return float(np.mean(ts))
+        f50_ms = timed_find(d_mixed)
+        f0_ms = timed_find(d_abs)
+        _, fs50 = table.find(d_mixed, d_out, want_stats=True)
+        _, fs0 = table.find(d_abs, d_out, want_stats=True)
+        assert fs0.hits == 0 and fs50.hits == half
+
+        peaks = load_peaks()
+        ins_bytes = bht.predict_sectors(KIND, B, outcome.mean_probes, bht.OP_INSERT) * 32 * n
+        find_bytes = bht.predict_sectors(KIND, B, fs100.mean_probes, bht.OP_FIND) * 32 * n
+        dom_insert = ins_ms >= find_ms
+        dom_bytes, dom_ms = (ins_bytes, ins_ms) if dom_insert else (find_bytes, find_ms)
+        roof = lambda by, ms: {"bound": "hbm", "achieved": by / (ms * 1e-3) / 1e9, "peak": peaks["hbm_gbs"],  # noqa: E731
+                               "unit": "GB/s", "frac": by / (ms * 1e-3) / 1e9 / peaks["hbm_gbs"], "traffic": None,
+                               "peak_source": peaks["source"]}
+        roofline = roof(dom_bytes, dom_ms)
+        roofline["kernel"] = "bulk_insert_cuckoo_kernel<16,3>" if dom_insert else "bulk_find_kernel<16,3,true>"
+        roofline["algorithmic_bytes_per_key"] = dom_bytes / n
+        roofline["frac_of_8TBps"] = dom_bytes / (dom_ms * 1e-3) / 8e12
+        detail = {
+            "clear_ms": clear_ms, "insert_ms": ins_ms, "find_ms": find_ms,
+            "insert_mkeys": n / ins_ms / 1e3, "find_100_mkeys": n / find_ms / 1e3,
+            "find_50_mkeys": n / f50_ms / 1e3, "find_0_mkeys": n / f0_ms / 1e3,
+            "insert_probes_per_key": outcome.mean_probes, "find_100_probes_per_key": fs100.mean_probes,
+            "find_50_probes_per_key": fs50.mean_probes, "find_0_probes_per_key": fs0.mean_probes,
+            "roofline_insert": roof(ins_bytes, ins_ms), "roofline_find_100": roof(find_bytes, find_ms),
+            "roofline_find_50": roof(bht.predict_sectors(KIND, B, fs50.mean_probes, bht.OP_FIND) * 32 * n, f50_ms),
+            "roofline_find_0": roof(bht.predict_sectors(KIND, B, fs0.mean_probes, bht.OP_FIND) * 32 * n, f0_ms),
+        }
+
+        # ---- e2e: the same pass through the C ABI with HOST buffers (pinned), copies inside the timed region
+        h_keys = torch.from_numpy(present.view(np.int32)).pin_memory()
+        h_vals = torch.from_numpy(values.view(np.int32)).pin_memory()
+        h_out = torch.empty(n, dtype=torch.int32).pin_memory()
+        e2e_steps = max(2, min(args.steps, 5))
+
+        def e2e_step():
+            table.clear()
+            o = table.insert(h_keys, h_vals)  # H2D of keys + values inside; result read back
+            table.find(h_keys, h_out)         # H2D of queries, D2H of answers inside
+            return o
+        e2e_step()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            o = e2e_step()
+        torch.cuda.synchronize()
+        e2e_s = (time.perf_counter() - t0) / e2e_steps
+        assert o.success and np.array_equal(h_out.numpy().view(np.uint32), values)
+        e2e = {"value": 2 * n / e2e_s / 1e6, "unit": "MKeys/s", "h2d_bytes_per_step": 12 * n,
+               "d2h_bytes_per_step": 4 * n + 64, "ms_per_step": e2e_s * 1e3,
+               "api": "bht_insert / bht_find with BHT_MEM_HOST (pinned host arrays, 3-slot staged PCIe pipeline)"}
+
+        cpu = cpu_baseline_leg(args, present, n) if not args.no_cpu_baseline else None
+        line = {
+            "metric": METRIC, "value": value, "unit": "MKeys/s", "n_gpus": 1, "steps": args.steps,
+            "warmup": max(args.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u32/u64 integer", "data": "synthetic: unique uniform u32 keys, MT19937",
+            "config": wl, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+            "clocks": clocks, "detail": detail,
+        }
+        print(json.dumps(line))
+        return 0
+
+    # ---- N > 1: sharded table, keys generated on the device, routing inside the timed region
+    keys, vals = bht.generate_unique_keys(SEED, rank * n, n, device=local)
+    keys, vals = keys.view(torch.int32), vals.view(torch.int32)
+    sharded = bht.ShardedTable(cfg, device=local, chunk=args.chunk)
+    out = torch.empty(n, dtype=torch.int32, device=device)
+
+    def step():
+        sharded.ops.table.clear()
+        o = sharded.insert(keys, vals)
+        sharded.find(keys, out)
+        return o
+
+    for _ in range(max(args.warmup, 3)):
+        o = step()
+    assert o.success, o
+    assert torch.equal(out, vals), "sharded find answers differ from the inserted values"
+    barrier()
+    launches0 = bht.kernel_launch_count()
+    sampler.start()
+    t_start, t_end = ev(), ev()
+    t_start.record(stream)
+    for _ in range(args.steps):
+        step()
+    t_end.record(stream)
+    barrier()
+    clocks = sampler.stop()
+    ms_step = max_over_ranks(t_start.elapsed_time(t_end) / args.steps)
+    launches = bht.kernel_launch_count() - launches0
+    if rank == 0:
+        value = 2 * n * world / (ms_step * 1e-3) / 1e6
+        line = {
+            "metric": METRIC, "value": value, "unit": "MKeys/s", "n_gpus": world, "steps": args.steps,
+            "warmup": max(args.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u32/u64 integer",
+            "data": "synthetic: unique u32 keys from a device-side bijection of a counter",
+            "config": wl, "roofline": None, "cpu_baseline": None,
+            "e2e": {"value": value, "unit": "MKeys/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 64,
+                    "note": "sharded pass: inputs are device-resident per rank; routing (NCCL all-to-all) is inside"},
+            "gpu_launches": int(launches), "clocks": clocks,
+        }
+        print(json.dumps(line))
+    dist.destroy_process_group()
+    return 0
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        p = json.load(open(path))
+        return {"hbm_gbs": float(p["hbm_gbs"]), "source": "MEASURED_PEAKS.json (measured copy bandwidth)"}
+    return {"hbm_gbs": 6650.0, "source": "fallback 6.65 TB/s (B200_PROFILING.md)"}
+
+
+def cpu_baseline_leg(args, present, n):
+    """The reference CPU implementation timed on this box's host cores, bounded to roughly 10-30 s."""
+    from oracle import binding
+    if not binding.ref_available():
+        return {"value": None, "unit": "MKeys/s", "cores": 0, "kind": "reference", "sample": "oracle/_ref not built"}
+    ref = binding.ref()
+    threads = ref.hardware_concurrency()
+    ocfg = make_ref_config(ref, n)
+    probe_n = min(n, 1_000_000)
+    tb, tf, _, _ = cpu_reference_pass(ref, ocfg, present, present, probe_n, threads)
+    rate = 2 * probe_n / max(tb + tf, 1e-9)
+    n_sample = int(min(n, max(1_000_000, rate * 20.0 / 2)))
+    tb, tf, out, hits = cpu_reference_pass(ref, ocfg, present, present, n_sample, threads)
+    assert out["success"] and hits == n_sample
+    return {"value": 2 * n_sample / (tb + tf) / 1e6, "unit": "MKeys/s", "cores": threads, "kind": "reference",
+            "insert_mkeys": n_sample / tb / 1e6, "find_mkeys": n_sample / tf / 1e6,
+            "sample": f"first {n_sample} of the {n} keys: reference build(parallel, {threads} workers) into the "
+                      f"full-size table + {n_sample} positive find_key calls over {threads} threads"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="cuda", choices=["cuda", "reference"])
+    ap.add_argument("--keys", type=int, default=N_KEYS, help="keys per GPU")
+    ap.add_argument("--chunk", type=int, default=1 << 24, help="sharded pipeline chunk (keys)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_cuda(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -153,6 +153,14 @@ bht_status bht_insert(bht_table* table, const uint32_t* keys, const uint32_t* va
 bht_status bht_find(const bht_table* table, const uint32_t* keys, uint32_t* out_values, uint64_t n,
                     int32_t mem_space, bht_find_result* result, void* stream);
 
+/* The reference's per-variant entry points bcht_insert / bp2ht_insert / iht_insert and bcht_find /
+ * bp2ht_find / iht_find (table.hpp:84-101): as bht_insert / bht_find, but BHT_KIND_MISMATCH when the
+ * table is not of `kind` (require_kind, table.cpp:15-17; BHT_BCHT also accepts a 1cht table). */
+bht_status bht_insert_as(bht_table* table, int32_t kind, const uint32_t* keys, const uint32_t* values,
+                         uint64_t n, int32_t mem_space, bht_insert_result* result, void* stream);
+bht_status bht_find_as(const bht_table* table, int32_t kind, const uint32_t* keys, uint32_t* out_values,
+                       uint64_t n, int32_t mem_space, bht_find_result* result, void* stream);
+
 /* bcht/1cht find without the early exit: bcht_find_no_early_exit (oracle.cpp:56-63). */
 bht_status bht_find_exhaustive(const bht_table* table, const uint32_t* keys, uint32_t* out_values,
                                uint64_t n, int32_t mem_space, bht_find_result* result, void* stream);
@@ -212,6 +220,15 @@ bht_status bht_shard_unpermute(const uint32_t* answers, const uint32_t* index, u
  * host-side rejection set.  Indices >= some n are guaranteed-absent negatives. */
 bht_status bht_generate_unique_keys(uint64_t seed, uint64_t offset, uint64_t n, uint32_t* out_keys,
                                     uint32_t* out_values, int32_t device, void* stream);
+
+/* The same bijection / value stream evaluated on the host for one counter / key. */
+uint32_t bht_unique_key_host(uint64_t seed, uint32_t counter);
+uint32_t bht_synthetic_value_host(uint64_t seed, uint32_t key);
+
+/* ---- pinned host buffers for BHT_MEM_HOST callers (cudaMallocHost / cudaFreeHost) --------- */
+
+bht_status bht_host_alloc(size_t bytes, void** out);
+bht_status bht_host_free(void* ptr);
 
 /* ---- diagnostics ------------------------------------------------------------------------- */
 

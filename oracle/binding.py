@@ -397,6 +397,11 @@ class RefTable(_Table):
         self.last_find_seconds = ns.value * 1e-9
         return out, int(hits), int(p.value)
 
+    def find_bulk_timed(self, keys, threads=1):
+        """-> (values, hits, probes, seconds of the find loop alone)"""
+        out, hits, probes = self.find_bulk(keys, threads)
+        return out, hits, probes, self.last_find_seconds
+
     def check_membership(self, keys, n_negative, seed):
         keys = _u32(keys)
         out = (C.c_uint64 * 3)()

@@ -1,0 +1,739 @@
+// capi.cu — the C ABI of include/bht_b200.h: C++ host code over the sm_100a kernels.
+//
+// Each entry point names the reference interface it replaces in include/bht_b200.h.  This file owns
+// what `class hash_table` owns in the reference (proj/include/bht/table.hpp:28-80): the config, the
+// slot store (device memory here) and the inserted counter; plus the staging pipeline that moves
+// host-resident key / value / answer arrays over PCIe in chunks while the probe kernels run.
+//
+// There is no CPU fallback anywhere in this file: without a usable device every compute entry point
+// returns BHT_CUDA_ERROR.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <string>
+
+#include "../../include/bht_b200.h"
+#include "kernels.h"
+
+using namespace bht_b200;
+
+namespace {
+
+thread_local std::string g_error;
+
+bht_status fail(bht_status s, const std::string& msg) {
+  g_error = msg;
+  return s;
+}
+bht_status cuda_fail(cudaError_t e, const char* what) {
+  g_error = std::string(what) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")";
+  return BHT_CUDA_ERROR;
+}
+#define BHT_CUDA(expr)                                        \
+  do {                                                        \
+    cudaError_t e__ = (expr);                                 \
+    if (e__ != cudaSuccess) return cuda_fail(e__, #expr);     \
+  } while (0)
+
+struct DeviceScope {  // every call runs on the table's device and leaves the caller's device as it was
+  int prev = -1;
+  bool switched = false;
+  cudaError_t err = cudaSuccess;
+  explicit DeviceScope(int device) {
+    err = cudaGetDevice(&prev);
+    if (err == cudaSuccess && prev != device) {
+      err = cudaSetDevice(device);
+      switched = err == cudaSuccess;
+    }
+  }
+  ~DeviceScope() {
+    if (switched) cudaSetDevice(prev);
+  }
+};
+#define BHT_ON_DEVICE(dev)       \
+  DeviceScope scope__(dev);      \
+  if (scope__.err != cudaSuccess) return cuda_fail(scope__.err, "cudaSetDevice")
+
+constexpr int kStageSlots = 3;
+constexpr uint64_t kStageChunk = 1ull << 22;  // keys per staged chunk: 16 MiB per array over PCIe
+constexpr uint64_t kFailedLogCap = 1ull << 20;
+constexpr uint32_t kRetryCap = 1024;
+
+// Host <-> device staging for BHT_MEM_HOST calls: kStageSlots chunks in flight, copy-in, probe kernel
+// and copy-out on three streams chained by events.
+struct Staging {
+  bool ready = false;
+  uint32_t* keys[kStageSlots] = {};
+  uint32_t* vals[kStageSlots] = {};  // values (insert) or answers (find)
+  cudaStream_t h2d = nullptr, d2h = nullptr, compute = nullptr;
+  cudaEvent_t in_done[kStageSlots] = {}, kernel_done[kStageSlots] = {}, out_done[kStageSlots] = {};
+};
+
+}  // namespace
+
+struct bht_table {
+  bht_config cfg{};
+  int device = 0;
+  int sm_count = 148;
+  TableView view{};
+  DevCounters* ctr = nullptr;       // device
+  DevCounters* ctr_host = nullptr;  // pinned mirror
+  uint32_t* failed_keys = nullptr;  // device log of dropped keys
+  uint64_t inserted_bound = 0;      // host upper bound on the device's inserted_total
+  Staging stage;
+  std::mutex mu;  // serialises calls that touch the counter block / staging buffers
+};
+
+namespace {
+
+uint32_t hash_count_of(int32_t kind) {
+  switch (kind) {
+    case BHT_ONE_CHT: return 4;
+    case BHT_BCHT: return 3;
+    case BHT_BP2HT: return 2;
+    case BHT_IHT: return 3;
+    default: return 0;
+  }
+}
+
+bool is_pow2(uint32_t x) { return x != 0 && (x & (x - 1)) == 0; }
+
+bht_status validate_config(const bht_config& c) {
+  const uint32_t h = hash_count_of(c.kind);
+  if (h == 0) return fail(BHT_INVALID_ARGUMENT, "bht_create: unknown table kind");
+  // hash_table::hash_table (table.cpp:22-23)
+  if (c.n_hashes != h) return fail(BHT_INVALID_ARGUMENT, "hash_table: config has the wrong number of hash functions");
+  if (!is_pow2(c.bucket_size) || c.bucket_size > BHT_MAX_BUCKET_SIZE)
+    return fail(BHT_INVALID_ARGUMENT, "bht_create: bucket_size must be a power of two in [1, 64]");
+  if (c.kind == BHT_ONE_CHT && c.bucket_size != 1) return fail(BHT_INVALID_ARGUMENT, "bht_create: 1cht requires bucket_size 1");
+  if (c.num_buckets == 0 || c.capacity != c.num_buckets * c.bucket_size)
+    return fail(BHT_INVALID_ARGUMENT, "bht_create: capacity must equal num_buckets * bucket_size > 0");
+  if (c.num_buckets > 0xFFFFFFFFull) return fail(BHT_INVALID_ARGUMENT, "bht_create: num_buckets must fit 32 bits");
+  if (c.kind == BHT_IHT && (c.threshold == 0 || c.threshold > c.bucket_size))
+    return fail(BHT_INVALID_ARGUMENT, "bht_create: iht threshold must be in [1, bucket_size]");
+  for (uint32_t i = 0; i < h; ++i) {
+    if (c.alpha[i] > 0xFFFFFFFFull || c.beta[i] > 0xFFFFFFFFull)
+      return fail(BHT_INVALID_ARGUMENT, "bht_create: hash constants must fit 32 bits (the reference draws them below p)");
+    if (c.range[i] == 0 || c.range[i] > c.num_buckets)
+      return fail(BHT_INVALID_ARGUMENT, "bht_create: hash range must be in [1, num_buckets]");
+  }
+  return BHT_OK;
+}
+
+cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+bht_status ensure_staging(bht_table* t) {
+  Staging& s = t->stage;
+  if (s.ready) return BHT_OK;
+  for (int i = 0; i < kStageSlots; ++i) {
+    BHT_CUDA(cudaMalloc(&s.keys[i], kStageChunk * sizeof(uint32_t)));
+    BHT_CUDA(cudaMalloc(&s.vals[i], kStageChunk * sizeof(uint32_t)));
+    BHT_CUDA(cudaEventCreateWithFlags(&s.in_done[i], cudaEventDisableTiming));
+    BHT_CUDA(cudaEventCreateWithFlags(&s.kernel_done[i], cudaEventDisableTiming));
+    BHT_CUDA(cudaEventCreateWithFlags(&s.out_done[i], cudaEventDisableTiming));
+  }
+  BHT_CUDA(cudaStreamCreateWithFlags(&s.h2d, cudaStreamNonBlocking));
+  BHT_CUDA(cudaStreamCreateWithFlags(&s.d2h, cudaStreamNonBlocking));
+  BHT_CUDA(cudaStreamCreateWithFlags(&s.compute, cudaStreamNonBlocking));
+  s.ready = true;
+  return BHT_OK;
+}
+
+void release_staging(Staging& s) {
+  for (int i = 0; i < kStageSlots; ++i) {
+    if (s.keys[i]) cudaFree(s.keys[i]);
+    if (s.vals[i]) cudaFree(s.vals[i]);
+    if (s.in_done[i]) cudaEventDestroy(s.in_done[i]);
+    if (s.kernel_done[i]) cudaEventDestroy(s.kernel_done[i]);
+    if (s.out_done[i]) cudaEventDestroy(s.out_done[i]);
+  }
+  if (s.h2d) cudaStreamDestroy(s.h2d);
+  if (s.d2h) cudaStreamDestroy(s.d2h);
+  if (s.compute) cudaStreamDestroy(s.compute);
+  s = Staging{};
+}
+
+bht_status read_counters(bht_table* t, cudaStream_t stream) {
+  BHT_CUDA(cudaMemcpyAsync(t->ctr_host, t->ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, stream));
+  BHT_CUDA(cudaStreamSynchronize(stream));
+  t->inserted_bound = t->ctr_host->inserted_total;
+  return BHT_OK;
+}
+
+void fill_insert_result(const bht_table* t, uint64_t attempted, bht_insert_result* r) {
+  const DevCounters& c = *t->ctr_host;
+  r->attempted = attempted;
+  r->inserted = c.inserted;
+  r->failed = c.failed;
+  r->probes = c.insert_probes;
+  r->first_failed_key = c.failed_key_tag ? c.failed_key_tag - 1u : BHT_EMPTY_KEY;
+  r->success = c.inserted == attempted ? 1u : 0u;
+}
+
+cudaError_t launch_insert_kind(const bht_table* t, const uint32_t* keys, const uint32_t* values, uint64_t n,
+                               cudaStream_t stream) {
+  switch (t->cfg.kind) {
+    case BHT_ONE_CHT:
+    case BHT_BCHT:
+      return launch_insert_cuckoo(t->view, keys, values, n, t->ctr, t->failed_keys, kFailedLogCap, t->sm_count, stream);
+    case BHT_BP2HT:
+      return launch_insert_p2(t->view, keys, values, n, t->ctr, t->failed_keys, kFailedLogCap, t->sm_count, stream);
+    case BHT_IHT:
+      return launch_insert_iht(t->view, keys, values, n, t->ctr, t->failed_keys, kFailedLogCap, t->sm_count, stream);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+bool kind_matches(int32_t table_kind, int32_t as_kind) {
+  // bcht_insert / bcht_find accept both cuckoo kinds (table.cpp:55,96)
+  const bool cuckoo = table_kind == BHT_ONE_CHT || table_kind == BHT_BCHT;
+  if (as_kind == BHT_BCHT || as_kind == BHT_ONE_CHT) return cuckoo;
+  return table_kind == as_kind;
+}
+
+bht_status do_insert(bht_table* t, const uint32_t* keys, const uint32_t* values, uint64_t n, int32_t mem_space,
+                     bht_insert_result* result, void* stream_v) {
+  if (t == nullptr) return fail(BHT_INVALID_ARGUMENT, "bht_insert: null table");
+  if (n != 0 && (keys == nullptr || values == nullptr)) return fail(BHT_INVALID_ARGUMENT, "bht_insert: null keys / values");
+  if (mem_space != BHT_MEM_DEVICE && mem_space != BHT_MEM_HOST) return fail(BHT_INVALID_ARGUMENT, "bht_insert: bad mem_space");
+  BHT_ON_DEVICE(t->device);
+  std::lock_guard<std::mutex> lock(t->mu);
+  cudaStream_t stream = as_stream(stream_v);
+
+  // build(): "key set exceeds table capacity" (table.cpp:225), against what is resident already
+  if (t->inserted_bound + n > t->cfg.capacity) {
+    bht_status s = read_counters(t, stream);
+    if (s != BHT_OK) return s;
+    if (t->inserted_bound + n > t->cfg.capacity) return fail(BHT_CAPACITY_EXCEEDED, "build: key set exceeds table capacity");
+  }
+
+  BHT_CUDA(cudaMemsetAsync(t->ctr, 0, kPerCallCounterBytes, stream));
+  if (mem_space == BHT_MEM_DEVICE) {
+    BHT_CUDA(launch_insert_kind(t, keys, values, n, stream));
+  } else if (n != 0) {
+    bht_status s = ensure_staging(t);
+    if (s != BHT_OK) return s;
+    Staging& st = t->stage;
+    cudaEvent_t start = st.out_done[0];  // reuse as the "counters are zeroed" marker
+    BHT_CUDA(cudaEventRecord(start, stream));
+    BHT_CUDA(cudaStreamWaitEvent(st.compute, start, 0));
+    const uint64_t chunks = (n + kStageChunk - 1) / kStageChunk;
+    for (uint64_t c = 0; c < chunks; ++c) {
+      const int slot = static_cast<int>(c % kStageSlots);
+      const uint64_t off = c * kStageChunk;
+      const uint64_t len = std::min(kStageChunk, n - off);
+      if (c >= kStageSlots) BHT_CUDA(cudaStreamWaitEvent(st.h2d, st.kernel_done[slot], 0));
+      BHT_CUDA(cudaMemcpyAsync(st.keys[slot], keys + off, len * sizeof(uint32_t), cudaMemcpyHostToDevice, st.h2d));
+      BHT_CUDA(cudaMemcpyAsync(st.vals[slot], values + off, len * sizeof(uint32_t), cudaMemcpyHostToDevice, st.h2d));
+      BHT_CUDA(cudaEventRecord(st.in_done[slot], st.h2d));
+      BHT_CUDA(cudaStreamWaitEvent(st.compute, st.in_done[slot], 0));
+      BHT_CUDA(launch_insert_kind(t, st.keys[slot], st.vals[slot], len, st.compute));
+      BHT_CUDA(cudaEventRecord(st.kernel_done[slot], st.compute));
+    }
+    BHT_CUDA(cudaStreamWaitEvent(stream, st.kernel_done[(chunks - 1) % kStageSlots], 0));
+    BHT_CUDA(cudaStreamSynchronize(stream));  // the caller's host arrays are free again on return
+  }
+  t->inserted_bound += n;
+  if (result != nullptr) {
+    bht_status s = read_counters(t, stream);
+    if (s != BHT_OK) return s;
+    fill_insert_result(t, n, result);
+  }
+  return BHT_OK;
+}
+
+bht_status do_find(const bht_table* ct, bool early_exit, const uint32_t* keys, uint32_t* out, uint64_t n,
+                   int32_t mem_space, bht_find_result* result, void* stream_v) {
+  if (ct == nullptr) return fail(BHT_INVALID_ARGUMENT, "bht_find: null table");
+  if (n != 0 && (keys == nullptr || out == nullptr)) return fail(BHT_INVALID_ARGUMENT, "bht_find: null keys / out_values");
+  if (mem_space != BHT_MEM_DEVICE && mem_space != BHT_MEM_HOST) return fail(BHT_INVALID_ARGUMENT, "bht_find: bad mem_space");
+  bht_table* t = const_cast<bht_table*>(ct);  // the counter block and staging buffers are scratch state
+  BHT_ON_DEVICE(t->device);
+  cudaStream_t stream = as_stream(stream_v);
+
+  if (mem_space == BHT_MEM_DEVICE && result == nullptr) {
+    // lock-free: concurrent finds on different streams share nothing but the read-only store
+    BHT_CUDA(launch_find(t->view, early_exit, keys, out, n, nullptr, t->sm_count, stream));
+    return BHT_OK;
+  }
+
+  std::lock_guard<std::mutex> lock(t->mu);
+  DevCounters* ctr = result != nullptr ? t->ctr : nullptr;
+  if (ctr != nullptr) BHT_CUDA(cudaMemsetAsync(t->ctr, 0, kPerCallCounterBytes, stream));
+  if (mem_space == BHT_MEM_DEVICE) {
+    BHT_CUDA(launch_find(t->view, early_exit, keys, out, n, ctr, t->sm_count, stream));
+  } else if (n != 0) {
+    bht_status s = ensure_staging(t);
+    if (s != BHT_OK) return s;
+    Staging& st = t->stage;
+    // everything already queued on the caller's stream (inserts, the counter reset) precedes the chunks
+    cudaEvent_t start = st.in_done[0];
+    BHT_CUDA(cudaEventRecord(start, stream));
+    BHT_CUDA(cudaStreamWaitEvent(st.compute, start, 0));
+    const uint64_t chunks = (n + kStageChunk - 1) / kStageChunk;
+    for (uint64_t c = 0; c < chunks; ++c) {
+      const int slot = static_cast<int>(c % kStageSlots);
+      const uint64_t off = c * kStageChunk;
+      const uint64_t len = std::min(kStageChunk, n - off);
+      if (c >= kStageSlots) {
+        BHT_CUDA(cudaStreamWaitEvent(st.h2d, st.kernel_done[slot], 0));   // keys[slot] consumed
+        BHT_CUDA(cudaStreamWaitEvent(st.compute, st.out_done[slot], 0));  // vals[slot] drained
+      }
+      BHT_CUDA(cudaMemcpyAsync(st.keys[slot], keys + off, len * sizeof(uint32_t), cudaMemcpyHostToDevice, st.h2d));
+      BHT_CUDA(cudaEventRecord(st.in_done[slot], st.h2d));
+      BHT_CUDA(cudaStreamWaitEvent(st.compute, st.in_done[slot], 0));
+      BHT_CUDA(launch_find(t->view, early_exit, st.keys[slot], st.vals[slot], len, ctr, t->sm_count, st.compute));
+      BHT_CUDA(cudaEventRecord(st.kernel_done[slot], st.compute));
+      BHT_CUDA(cudaStreamWaitEvent(st.d2h, st.kernel_done[slot], 0));
+      BHT_CUDA(cudaMemcpyAsync(out + off, st.vals[slot], len * sizeof(uint32_t), cudaMemcpyDeviceToHost, st.d2h));
+      BHT_CUDA(cudaEventRecord(st.out_done[slot], st.d2h));
+    }
+    BHT_CUDA(cudaStreamWaitEvent(stream, st.kernel_done[(chunks - 1) % kStageSlots], 0));
+    BHT_CUDA(cudaStreamSynchronize(st.d2h));  // answers are in the caller's host array on return
+    BHT_CUDA(cudaStreamSynchronize(stream));
+  }
+  if (result != nullptr) {
+    bht_status s = read_counters(t, stream);
+    if (s != BHT_OK) return s;
+    result->queries = n;
+    result->hits = t->ctr_host->find_hits;
+    result->probes = t->ctr_host->find_probes;
+    result->value_sum = t->ctr_host->find_value_sum;
+  }
+  return BHT_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+// ---- configuration ------------------------------------------------------------------------------
+
+uint32_t bht_hash_count(int32_t kind) { return hash_count_of(kind); }
+
+uint32_t bht_default_max_chain(uint64_t n_keys) {
+  // default_max_chain (core.cpp:28-31): max(7 * ceil(log2 n), 128), ceil(log2 n) = bit_width(n - 1)
+  uint32_t log2n = 1;
+  if (n_keys > 1) {
+    log2n = 0;
+    for (uint64_t v = n_keys - 1; v != 0; v >>= 1) ++log2n;
+  }
+  return std::max<uint32_t>(7u * log2n, 128u);
+}
+
+uint64_t bht_mix_seed(uint64_t seed, uint64_t stream) { return mix_seed(seed, stream); }
+
+uint64_t bht_bucket_index_host(uint64_t alpha, uint64_t beta, uint64_t range, uint32_t key) {
+  if (alpha > 0xFFFFFFFFull || beta > 0xFFFFFFFFull || range == 0 || range > 0xFFFFFFFFull) {
+    g_error = "bht_bucket_index_host: alpha, beta and range must fit 32 bits, range > 0";
+    return ~0ull;
+  }
+  return bucket_index(make_hash_fn(alpha, beta, range), key);
+}
+
+uint32_t bht_value_for_key(uint32_t key) {
+  // value_for_key (keygen.hpp:23-26): k ^ 0x5A5A5A5A; the one image that hits the sentinel is masked
+  const uint32_t v = key ^ 0x5A5A5A5Au;
+  return v == BHT_EMPTY_VALUE ? (v & 0x7FFFFFFFu) : v;
+}
+
+double bht_predict_sectors(int32_t kind, uint32_t bucket_size, double mean_probes, int32_t op) {
+  // sector_model.hpp:18-31: a bucket read costs ceil(8b/32) sectors, 2 for 1cht (DRAM-to-L2 granularity is
+  // 64 bytes); an insert adds the one sector its atomic writes back.
+  const double per_probe = kind == BHT_ONE_CHT ? 2.0 : static_cast<double>((bucket_size * 8u + 31u) / 32u);
+  return mean_probes * per_probe + (op == 0 ? 1.0 : 0.0);
+}
+
+bht_status bht_make_config(int32_t kind, uint64_t n_keys, double lf, uint32_t bucket_size, int64_t threshold,
+                           uint64_t seed, int64_t max_chain, bht_config* out) {
+  if (out == nullptr) return fail(BHT_INVALID_ARGUMENT, "make_config: null output");
+  if (hash_count_of(kind) == 0) return fail(BHT_INVALID_ARGUMENT, "make_config: unknown table kind");
+  // core.cpp:40-46, same order and messages
+  if (n_keys == 0) return fail(BHT_INVALID_ARGUMENT, "make_config: n_keys must be positive");
+  if (!(lf > 0.0) || lf > 1.0) return fail(BHT_INVALID_ARGUMENT, "make_config: load factor must be in (0, 1]");
+  if (!is_pow2(bucket_size) || bucket_size > BHT_MAX_BUCKET_SIZE)
+    return fail(BHT_INVALID_ARGUMENT, "make_config: bucket_size must be a power of two in [1, 64]");
+  if (kind == BHT_ONE_CHT && bucket_size != 1) return fail(BHT_INVALID_ARGUMENT, "make_config: 1cht requires bucket_size 1");
+
+  bht_config c;
+  std::memset(&c, 0, sizeof c);
+  c.kind = kind;
+  c.bucket_size = bucket_size;
+  c.num_buckets = static_cast<uint64_t>(std::ceil(static_cast<double>(n_keys) / (lf * static_cast<double>(bucket_size))));
+  c.capacity = c.num_buckets * bucket_size;
+  c.seed = seed;
+  c.n_hashes = hash_count_of(kind);
+  if (kind == BHT_IHT) {
+    c.threshold = threshold >= 0 ? static_cast<uint32_t>(threshold) : bucket_size * 80u / 100u;
+    if (c.threshold > bucket_size) return fail(BHT_INVALID_ARGUMENT, "make_config: threshold exceeds bucket_size");
+    if (c.threshold == 0) return fail(BHT_INVALID_ARGUMENT, "make_config: iht threshold must be positive");
+  }
+  if (kind == BHT_ONE_CHT || kind == BHT_BCHT)
+    c.max_chain = max_chain >= 0 ? static_cast<uint32_t>(max_chain) : bht_default_max_chain(n_keys);
+
+  // draw_hash_params (keygen.cpp:14-26) on xorshift_rng(mix_seed(seed, 0x68617368)) (core.cpp:65-66)
+  uint64_t rng = xorshift_init(mix_seed(seed, 0x68617368ull));
+  const uint32_t p = static_cast<uint32_t>(BHT_HASH_PRIME);
+  for (uint32_t i = 0; i < c.n_hashes; ++i) {
+    c.alpha[i] = 1ull + xorshift_next_below(rng, p - 1u);
+    c.beta[i] = xorshift_next_below(rng, p);
+    c.range[i] = c.num_buckets;
+  }
+  *out = c;
+  return BHT_OK;
+}
+
+// ---- lifetime -----------------------------------------------------------------------------------
+
+bht_status bht_create(const bht_config* cfg, int32_t device, bht_table** out) {
+  if (cfg == nullptr || out == nullptr) return fail(BHT_INVALID_ARGUMENT, "bht_create: null argument");
+  *out = nullptr;
+  bht_status vs = validate_config(*cfg);
+  if (vs != BHT_OK) return vs;
+  int n_dev = 0;
+  BHT_CUDA(cudaGetDeviceCount(&n_dev));
+  if (device < 0 || device >= n_dev) return fail(BHT_CUDA_ERROR, "bht_create: no such CUDA device");
+  BHT_ON_DEVICE(device);
+
+  bht_table* t = new (std::nothrow) bht_table();
+  if (t == nullptr) return fail(BHT_INVALID_ARGUMENT, "bht_create: out of host memory");
+  t->cfg = *cfg;
+  t->device = device;
+  cudaDeviceProp prop;
+  cudaError_t e = cudaGetDeviceProperties(&prop, device);
+  if (e == cudaSuccess && prop.major < 10) {
+    delete t;
+    return fail(BHT_CUDA_ERROR, "bht_create: kernels are built for sm_100a only; this device is older");
+  }
+  if (e == cudaSuccess) t->sm_count = prop.multiProcessorCount;
+
+  uint64_t* store = nullptr;
+  if (e == cudaSuccess) e = cudaMalloc(&store, cfg->capacity * sizeof(uint64_t));  // cudaMalloc aligns to >= 256 B
+  if (e == cudaSuccess) e = cudaMalloc(&t->ctr, sizeof(DevCounters));
+  if (e == cudaSuccess) e = cudaMallocHost(&t->ctr_host, sizeof(DevCounters));
+  if (e == cudaSuccess) e = cudaMalloc(&t->failed_keys, kFailedLogCap * sizeof(uint32_t));
+  if (e == cudaSuccess) e = cudaMemset(t->ctr, 0, sizeof(DevCounters));
+  if (e == cudaSuccess) e = launch_fill_empty(store, cfg->capacity, t->sm_count, nullptr);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(nullptr);
+  if (e != cudaSuccess) {
+    if (store) cudaFree(store);
+    if (t->ctr) cudaFree(t->ctr);
+    if (t->ctr_host) cudaFreeHost(t->ctr_host);
+    if (t->failed_keys) cudaFree(t->failed_keys);
+    delete t;
+    return cuda_fail(e, "bht_create");
+  }
+
+  TableView& v = t->view;
+  v.store = store;
+  for (uint32_t i = 0; i < cfg->n_hashes; ++i) v.h[i] = make_hash_fn(cfg->alpha[i], cfg->beta[i], cfg->range[i]);
+  for (uint32_t i = cfg->n_hashes; i < 4; ++i) v.h[i] = make_hash_fn(1, 0, 1);
+  v.num_buckets = cfg->num_buckets;
+  v.seed = cfg->seed;
+  v.n_hashes = cfg->n_hashes;
+  v.bucket_size = cfg->bucket_size;
+  v.threshold = cfg->threshold;
+  v.max_chain = cfg->max_chain;
+  v.prose = 0;
+  v.retry_cap = kRetryCap;
+  *out = t;
+  return BHT_OK;
+}
+
+bht_status bht_destroy(bht_table* t) {
+  if (t == nullptr) return BHT_OK;
+  BHT_ON_DEVICE(t->device);
+  cudaDeviceSynchronize();
+  release_staging(t->stage);
+  cudaFree(t->view.store);
+  cudaFree(t->ctr);
+  cudaFreeHost(t->ctr_host);
+  cudaFree(t->failed_keys);
+  delete t;
+  return BHT_OK;
+}
+
+bht_status bht_clear(bht_table* t, void* stream) {
+  if (t == nullptr) return fail(BHT_INVALID_ARGUMENT, "bht_clear: null table");
+  BHT_ON_DEVICE(t->device);
+  std::lock_guard<std::mutex> lock(t->mu);
+  BHT_CUDA(launch_fill_empty(t->view.store, t->cfg.capacity, t->sm_count, as_stream(stream)));
+  BHT_CUDA(cudaMemsetAsync(t->ctr, 0, sizeof(DevCounters), as_stream(stream)));
+  t->inserted_bound = 0;
+  return BHT_OK;
+}
+
+bht_status bht_get_config(const bht_table* t, bht_config* out) {
+  if (t == nullptr || out == nullptr) return fail(BHT_INVALID_ARGUMENT, "bht_get_config: null argument");
+  *out = t->cfg;
+  return BHT_OK;
+}
+
+int32_t bht_device_of(const bht_table* t) { return t ? t->device : -1; }
+
+// ---- the hot path -------------------------------------------------------------------------------
+
+bht_status bht_insert(bht_table* t, const uint32_t* keys, const uint32_t* values, uint64_t n, int32_t mem_space,
+                      bht_insert_result* result, void* stream) {
+  return do_insert(t, keys, values, n, mem_space, result, stream);
+}
+
+bht_status bht_insert_as(bht_table* t, int32_t kind, const uint32_t* keys, const uint32_t* values, uint64_t n,
+                         int32_t mem_space, bht_insert_result* result, void* stream) {
+  if (t == nullptr) return fail(BHT_INVALID_ARGUMENT, "bht_insert_as: null table");
+  if (!kind_matches(t->cfg.kind, kind)) return fail(BHT_KIND_MISMATCH, "insert: table kind does not match the variant");
+  return do_insert(t, keys, values, n, mem_space, result, stream);
+}
+
+bht_status bht_find(const bht_table* t, const uint32_t* keys, uint32_t* out, uint64_t n, int32_t mem_space,
+                    bht_find_result* result, void* stream) {
+  const bool cuckoo = t != nullptr && (t->cfg.kind == BHT_ONE_CHT || t->cfg.kind == BHT_BCHT);
+  return do_find(t, cuckoo, keys, out, n, mem_space, result, stream);
+}
+
+bht_status bht_find_as(const bht_table* t, int32_t kind, const uint32_t* keys, uint32_t* out, uint64_t n,
+                       int32_t mem_space, bht_find_result* result, void* stream) {
+  if (t == nullptr) return fail(BHT_INVALID_ARGUMENT, "bht_find_as: null table");
+  if (!kind_matches(t->cfg.kind, kind)) return fail(BHT_KIND_MISMATCH, "find: table kind does not match the variant");
+  return bht_find(t, keys, out, n, mem_space, result, stream);
+}
+
+bht_status bht_find_exhaustive(const bht_table* t, const uint32_t* keys, uint32_t* out, uint64_t n, int32_t mem_space,
+                               bht_find_result* result, void* stream) {
+  return do_find(t, false, keys, out, n, mem_space, result, stream);
+}
+
+bht_status bht_last_insert_result(bht_table* t, bht_insert_result* out, void* stream) {
+  if (t == nullptr || out == nullptr) return fail(BHT_INVALID_ARGUMENT, "bht_last_insert_result: null argument");
+  BHT_ON_DEVICE(t->device);
+  std::lock_guard<std::mutex> lock(t->mu);
+  bht_status s = read_counters(t, as_stream(stream));
+  if (s != BHT_OK) return s;
+  const DevCounters& c = *t->ctr_host;
+  fill_insert_result(t, c.inserted + c.failed, out);
+  return BHT_OK;
+}
+
+bht_status bht_failed_keys(bht_table* t, uint32_t* host_out, uint64_t max_keys, uint64_t* count) {
+  if (t == nullptr || count == nullptr) return fail(BHT_INVALID_ARGUMENT, "bht_failed_keys: null argument");
+  BHT_ON_DEVICE(t->device);
+  std::lock_guard<std::mutex> lock(t->mu);
+  BHT_CUDA(cudaDeviceSynchronize());
+  bht_status s = read_counters(t, nullptr);
+  if (s != BHT_OK) return s;
+  *count = t->ctr_host->failed_recorded;
+  const uint64_t n = std::min<uint64_t>(std::min<uint64_t>(*count, kFailedLogCap), max_keys);
+  if (n != 0 && host_out != nullptr)
+    BHT_CUDA(cudaMemcpy(host_out, t->failed_keys, n * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+  return BHT_OK;
+}
+
+bht_status bht_set_iht_prose_fallback(bht_table* t, int32_t enabled) {
+  if (t == nullptr) return fail(BHT_INVALID_ARGUMENT, "bht_set_iht_prose_fallback: null table");
+  if (t->cfg.kind != BHT_IHT) return fail(BHT_KIND_MISMATCH, "iht_insert: table kind does not match the variant");
+  t->view.prose = enabled ? 1u : 0u;
+  return BHT_OK;
+}
+
+// ---- load factor / store access -----------------------------------------------------------------
+
+bht_status bht_load_factor(const bht_table* ct, uint64_t* inserted, uint64_t* capacity) {
+  if (ct == nullptr) return fail(BHT_INVALID_ARGUMENT, "bht_load_factor: null table");
+  bht_table* t = const_cast<bht_table*>(ct);
+  BHT_ON_DEVICE(t->device);
+  std::lock_guard<std::mutex> lock(t->mu);
+  BHT_CUDA(cudaDeviceSynchronize());
+  bht_status s = read_counters(t, nullptr);
+  if (s != BHT_OK) return s;
+  if (inserted) *inserted = t->ctr_host->inserted_total;
+  if (capacity) *capacity = t->cfg.capacity;
+  return BHT_OK;
+}
+
+bht_status bht_count_occupied(const bht_table* ct, uint64_t* occupied, void* stream) {
+  if (ct == nullptr || occupied == nullptr) return fail(BHT_INVALID_ARGUMENT, "bht_count_occupied: null argument");
+  bht_table* t = const_cast<bht_table*>(ct);
+  BHT_ON_DEVICE(t->device);
+  std::lock_guard<std::mutex> lock(t->mu);
+  BHT_CUDA(launch_count_occupied(t->view.store, t->cfg.capacity, &t->ctr->scratch, t->sm_count, as_stream(stream)));
+  bht_status s = read_counters(t, as_stream(stream));
+  if (s != BHT_OK) return s;
+  *occupied = t->ctr_host->scratch;
+  return BHT_OK;
+}
+
+bht_status bht_count_inadmissible(const bht_table* ct, uint64_t* violations, void* stream) {
+  if (ct == nullptr || violations == nullptr) return fail(BHT_INVALID_ARGUMENT, "bht_count_inadmissible: null argument");
+  bht_table* t = const_cast<bht_table*>(ct);
+  BHT_ON_DEVICE(t->device);
+  std::lock_guard<std::mutex> lock(t->mu);
+  BHT_CUDA(launch_count_inadmissible(t->view, &t->ctr->scratch, t->sm_count, as_stream(stream)));
+  bht_status s = read_counters(t, as_stream(stream));
+  if (s != BHT_OK) return s;
+  *violations = t->ctr_host->scratch;
+  return BHT_OK;
+}
+
+bht_status bht_download_store(const bht_table* t, uint64_t* host_dst, void* stream) {
+  if (t == nullptr || host_dst == nullptr) return fail(BHT_INVALID_ARGUMENT, "bht_download_store: null argument");
+  BHT_ON_DEVICE(t->device);
+  BHT_CUDA(cudaMemcpyAsync(host_dst, t->view.store, t->cfg.capacity * sizeof(uint64_t), cudaMemcpyDeviceToHost,
+                           as_stream(stream)));
+  BHT_CUDA(cudaStreamSynchronize(as_stream(stream)));
+  return BHT_OK;
+}
+
+bht_status bht_upload_store(bht_table* t, const uint64_t* host_src, void* stream) {
+  if (t == nullptr || host_src == nullptr) return fail(BHT_INVALID_ARGUMENT, "bht_upload_store: null argument");
+  BHT_ON_DEVICE(t->device);
+  std::lock_guard<std::mutex> lock(t->mu);
+  cudaStream_t s = as_stream(stream);
+  BHT_CUDA(cudaMemcpyAsync(t->view.store, host_src, t->cfg.capacity * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
+  BHT_CUDA(cudaMemsetAsync(t->ctr, 0, sizeof(DevCounters), s));
+  BHT_CUDA(launch_count_occupied(t->view.store, t->cfg.capacity, &t->ctr->inserted_total, t->sm_count, s));
+  return read_counters(t, s);
+}
+
+bht_status bht_dump_store(const bht_table* t, const char* path) {
+  if (t == nullptr || path == nullptr) return fail(BHT_INVALID_ARGUMENT, "bht_dump_store: null argument");
+  const uint64_t n = t->cfg.capacity;
+  uint64_t* host = static_cast<uint64_t*>(std::malloc(n * sizeof(uint64_t)));
+  if (host == nullptr) return fail(BHT_IO_ERROR, "dump_store: out of host memory");
+  bht_status s = bht_download_store(t, host, nullptr);
+  if (s != BHT_OK) {
+    std::free(host);
+    return s;
+  }
+  std::FILE* f = std::fopen(path, "wb");
+  if (f == nullptr) {
+    std::free(host);
+    return fail(BHT_IO_ERROR, std::string("dump_store: cannot open ") + path);
+  }
+  // little-endian u64 per slot in bucket order (table.cpp:41-51); every supported host is little-endian
+  const bool ok = std::fwrite(host, sizeof(uint64_t), n, f) == n;
+  const bool closed = std::fclose(f) == 0;
+  std::free(host);
+  if (!ok || !closed) return fail(BHT_IO_ERROR, std::string("dump_store: write failed for ") + path);
+  return BHT_OK;
+}
+
+uint64_t* bht_device_store(const bht_table* t) { return t ? t->view.store : nullptr; }
+
+// ---- hash stage in isolation ----------------------------------------------------------------------
+
+bht_status bht_hash_keys(uint64_t alpha, uint64_t beta, uint64_t range, const uint32_t* keys, uint32_t* out, uint64_t n,
+                         int32_t mem_space, int32_t device, void* stream) {
+  if (alpha > 0xFFFFFFFFull || beta > 0xFFFFFFFFull || range == 0 || range > 0xFFFFFFFFull)
+    return fail(BHT_INVALID_ARGUMENT, "bht_hash_keys: alpha, beta and range must fit 32 bits, range > 0");
+  if (n != 0 && (keys == nullptr || out == nullptr)) return fail(BHT_INVALID_ARGUMENT, "bht_hash_keys: null argument");
+  BHT_ON_DEVICE(device);
+  cudaDeviceProp prop;
+  BHT_CUDA(cudaGetDeviceProperties(&prop, device));
+  const HashFn h = make_hash_fn(alpha, beta, range);
+  cudaStream_t s = as_stream(stream);
+  if (mem_space == BHT_MEM_DEVICE) {
+    BHT_CUDA(launch_hash_keys(h, keys, out, n, prop.multiProcessorCount, s));
+    return BHT_OK;
+  }
+  if (n == 0) return BHT_OK;
+  uint32_t *dk = nullptr, *dout = nullptr;
+  BHT_CUDA(cudaMalloc(&dk, n * sizeof(uint32_t)));
+  cudaError_t e = cudaMalloc(&dout, n * sizeof(uint32_t));
+  if (e == cudaSuccess) e = cudaMemcpyAsync(dk, keys, n * sizeof(uint32_t), cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = launch_hash_keys(h, dk, dout, n, prop.multiProcessorCount, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(out, dout, n * sizeof(uint32_t), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  cudaFree(dk);
+  if (dout) cudaFree(dout);
+  if (e != cudaSuccess) return cuda_fail(e, "bht_hash_keys");
+  return BHT_OK;
+}
+
+// ---- sharded table: routing -------------------------------------------------------------------------
+
+uint32_t bht_shard_of_host(uint64_t alpha, uint64_t beta, uint32_t n_shards, uint32_t key) {
+  return shard_of(static_cast<uint32_t>(alpha), static_cast<uint32_t>(beta), n_shards, key);
+}
+
+bht_status bht_shard_partition(uint64_t alpha, uint64_t beta, uint32_t n_shards, const uint32_t* keys,
+                               const uint32_t* values, uint64_t n, uint32_t* out_keys, uint32_t* out_values,
+                               uint32_t* out_index, uint64_t* counts_host, int32_t device, void* stream) {
+  if (alpha > 0xFFFFFFFFull || beta > 0xFFFFFFFFull) return fail(BHT_INVALID_ARGUMENT, "bht_shard_partition: constants must fit 32 bits");
+  if (n_shards == 0 || n_shards > static_cast<uint32_t>(kMaxShards))
+    return fail(BHT_INVALID_ARGUMENT, "bht_shard_partition: n_shards must be in [1, 256]");
+  if (n > 0xFFFFFFFFull) return fail(BHT_INVALID_ARGUMENT, "bht_shard_partition: at most 2^32 - 1 elements per call");
+  if (counts_host == nullptr || (n != 0 && (keys == nullptr || out_keys == nullptr)) || (values != nullptr && out_values == nullptr))
+    return fail(BHT_INVALID_ARGUMENT, "bht_shard_partition: null argument");
+  BHT_ON_DEVICE(device);
+  cudaDeviceProp prop;
+  BHT_CUDA(cudaGetDeviceProperties(&prop, device));
+  cudaStream_t s = as_stream(stream);
+  unsigned long long* scratch = nullptr;  // [counts | cursors]
+  BHT_CUDA(cudaMallocAsync(&scratch, 2 * sizeof(unsigned long long) * n_shards, s));
+  const uint32_t a = static_cast<uint32_t>(alpha), b = static_cast<uint32_t>(beta);
+  cudaError_t e = launch_shard_histogram(a, b, n_shards, keys, n, scratch, prop.multiProcessorCount, s);
+  if (e == cudaSuccess)
+    e = launch_shard_scatter(a, b, n_shards, keys, values, n, scratch, scratch + n_shards, out_keys, out_values, out_index,
+                             prop.multiProcessorCount, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(counts_host, scratch, sizeof(uint64_t) * n_shards, cudaMemcpyDeviceToHost, s);
+  cudaFreeAsync(scratch, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_fail(e, "bht_shard_partition");
+  return BHT_OK;
+}
+
+bht_status bht_shard_unpermute(const uint32_t* answers, const uint32_t* index, uint64_t n, uint32_t* out, int32_t device,
+                               void* stream) {
+  if (n != 0 && (answers == nullptr || index == nullptr || out == nullptr))
+    return fail(BHT_INVALID_ARGUMENT, "bht_shard_unpermute: null argument");
+  BHT_ON_DEVICE(device);
+  cudaDeviceProp prop;
+  BHT_CUDA(cudaGetDeviceProperties(&prop, device));
+  BHT_CUDA(launch_unpermute(answers, index, n, out, prop.multiProcessorCount, as_stream(stream)));
+  return BHT_OK;
+}
+
+// ---- synthetic workload ------------------------------------------------------------------------------
+
+bht_status bht_generate_unique_keys(uint64_t seed, uint64_t offset, uint64_t n, uint32_t* out_keys, uint32_t* out_values,
+                                    int32_t device, void* stream) {
+  if (n != 0 && out_keys == nullptr) return fail(BHT_INVALID_ARGUMENT, "bht_generate_unique_keys: null output");
+  if (offset + n > 0xFFFFFFFFull || offset + n < offset)
+    return fail(BHT_INVALID_ARGUMENT, "bht_generate_unique_keys: offset + n exceeds the 2^32 - 1 user keys");
+  BHT_ON_DEVICE(device);
+  cudaDeviceProp prop;
+  BHT_CUDA(cudaGetDeviceProperties(&prop, device));
+  BHT_CUDA(launch_generate_keys(seed, offset, n, out_keys, out_values, prop.multiProcessorCount, as_stream(stream)));
+  return BHT_OK;
+}
+
+uint32_t bht_unique_key_host(uint64_t seed, uint32_t counter) {
+  return unique_key(static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32), counter);
+}
+uint32_t bht_synthetic_value_host(uint64_t seed, uint32_t key) { return synthetic_value(static_cast<uint32_t>(seed >> 32), key); }
+
+// ---- pinned host buffers for BHT_MEM_HOST callers -----------------------------------------------------
+
+bht_status bht_host_alloc(size_t bytes, void** out) {
+  if (out == nullptr) return fail(BHT_INVALID_ARGUMENT, "bht_host_alloc: null output");
+  BHT_CUDA(cudaMallocHost(out, bytes));
+  return BHT_OK;
+}
+bht_status bht_host_free(void* p) {
+  if (p != nullptr) BHT_CUDA(cudaFreeHost(p));
+  return BHT_OK;
+}
+
+// ---- diagnostics -------------------------------------------------------------------------------------
+
+const char* bht_last_error_string(void) { return g_error.c_str(); }
+const char* bht_version_string(void) { return "bht_b200 0.1 (sm_100a)"; }
+uint64_t bht_kernel_launch_count(void) { return launch_count(); }
+size_t bht_sizeof_config(void) { return sizeof(bht_config); }
+
+}  // extern "C"

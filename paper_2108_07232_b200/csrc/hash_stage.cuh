@@ -88,4 +88,28 @@ __host__ __device__ __forceinline__ uint32_t xorshift_next_below(uint64_t& state
   return static_cast<uint32_t>(((x >> 32) * bound) >> 32);
 }
 
+// Synthetic workload (bht_generate_unique_keys): a keyed bijection of the 32-bit counter, every step
+// invertible mod 2^32, cycle-walked once past the sentinel so that counters [0, 2^32-2] map one-to-one
+// onto user keys [0, 2^32-2] (the key universe of core.hpp:23-24) without keygen.cpp's rejection set.
+__host__ __device__ __forceinline__ uint32_t mix32(uint32_t k0, uint32_t k1, uint32_t x) {
+  x ^= k0;
+  x ^= x >> 16;
+  x *= 0x85EBCA6Bu;
+  x ^= x >> 13;
+  x += k1;
+  x *= 0xC2B2AE35u;
+  x ^= x >> 16;
+  return x;
+}
+__host__ __device__ __forceinline__ uint32_t unique_key(uint32_t k0, uint32_t k1, uint32_t counter) {
+  uint32_t y = mix32(k0, k1, counter);
+  if (y == kEmptyKey) y = mix32(k0, k1, y);  // the sentinel is no fixed point unless nothing maps to it
+  return y;
+}
+// A value stream independent of the key bijection, never the sentinel.
+__host__ __device__ __forceinline__ uint32_t synthetic_value(uint32_t k1, uint32_t key) {
+  const uint32_t v = mix32(k1 ^ 0x9E3779B9u, 0x7F4A7C15u, key);
+  return v == kEmptyKey ? 0x5A5A5A5Au : v;
+}
+
 }  // namespace bht_b200

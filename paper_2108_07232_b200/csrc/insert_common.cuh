@@ -11,7 +11,7 @@ constexpr int kInsertBlock = 256;
 __device__ __forceinline__ void record_failed(DevCounters* ctr, uint32_t* failed_keys, uint64_t failed_cap, uint32_t key) {
   const unsigned long long pos = atomicAdd(&ctr->failed_recorded, 1ull);
   if (pos < failed_cap) failed_keys[pos] = key;
-  atomicMin(&ctr->first_failed_key, key);
+  atomicMax(&ctr->failed_key_tag, key + 1u);
 }
 
 __device__ __forceinline__ void flush_insert_counters(DevCounters* ctr, int lane, uint32_t n_ins, uint32_t n_fail,

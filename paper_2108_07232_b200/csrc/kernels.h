@@ -39,8 +39,9 @@ constexpr int kMaxShards = 256;
 cudaError_t launch_shard_histogram(uint32_t alpha, uint32_t beta, uint32_t n_shards, const uint32_t* keys, uint64_t n,
                                    unsigned long long* counts, int sm_count, cudaStream_t stream);
 cudaError_t launch_shard_scatter(uint32_t alpha, uint32_t beta, uint32_t n_shards, const uint32_t* keys,
-                                 const uint32_t* values, uint64_t n, unsigned long long* cursors, uint32_t* out_keys,
-                                 uint32_t* out_values, uint32_t* out_index, int sm_count, cudaStream_t stream);
+                                 const uint32_t* values, uint64_t n, const unsigned long long* counts,
+                                 unsigned long long* cursors, uint32_t* out_keys, uint32_t* out_values,
+                                 uint32_t* out_index, int sm_count, cudaStream_t stream);
 cudaError_t launch_unpermute(const uint32_t* answers, const uint32_t* index, uint64_t n, uint32_t* out, int sm_count,
                              cudaStream_t stream);
 cudaError_t launch_generate_keys(uint64_t seed, uint64_t offset, uint64_t n, uint32_t* keys, uint32_t* values,

@@ -272,18 +272,21 @@ struct TableView {
 };
 
 struct DevCounters {
-  unsigned long long inserted;        // this call
-  unsigned long long failed;          // this call
-  unsigned long long insert_probes;   // this call
-  unsigned long long find_hits;       // this call
-  unsigned long long find_probes;     // this call
-  unsigned long long find_value_sum;  // this call
-  unsigned long long scratch;         // count_occupied / inadmissible result
-  unsigned long long failed_recorded; // since clear: entries appended to the failed-key log
-  unsigned long long inserted_total;  // since clear
-  unsigned int first_failed_key;      // this call
+  // ---- per call: zeroed at the start of every bht_insert / bht_find ----
+  unsigned long long inserted;
+  unsigned long long failed;
+  unsigned long long insert_probes;
+  unsigned long long find_hits;
+  unsigned long long find_probes;
+  unsigned long long find_value_sum;
+  unsigned int failed_key_tag;  // max over dropped keys of key + 1; 0 = none dropped
   unsigned int pad;
+  // ---- since bht_clear / bht_upload_store ----
+  unsigned long long scratch;          // count_occupied / count_inadmissible result
+  unsigned long long failed_recorded;  // entries appended to the failed-key log
+  unsigned long long inserted_total;
 };
+constexpr size_t kPerCallCounterBytes = 7 * sizeof(unsigned long long);
 
 __device__ __forceinline__ unsigned long long warp_sum(unsigned long long v) {
 #pragma unroll
