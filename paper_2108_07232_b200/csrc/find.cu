@@ -9,60 +9,88 @@
 // Probe counts are identical to the reference's (one per bucket read), so the algorithmic bytes of
 // a launch are probes x ceil(8b/32) x 32 B (sector_model.hpp:18-31).
 //
-// Bound: HBM, random 128-byte lines.  Each warp owns 32 keys per batch; probe round i hashes the
-// still-pending keys with H_i and reads their buckets through the batched probe engine.
+// Bound: HBM, random 128-byte lines.  Each lane carries one query through its probe sequence
+// (state: key, position, next hash index); a lane whose query is answered takes the next query of
+// the warp's slice, so each round of a warp is 32 independent bucket fetches.
 #include "kernels.h"
 
 namespace bht_b200 {
 
-constexpr int kFindBlock = 256;
-
 template <int B, int H, bool EARLY_EXIT>
-__global__ void __launch_bounds__(kFindBlock)
+__global__ void __launch_bounds__(block_threads<B>(1))
 bulk_find_kernel(const __grid_constant__ TableView t, const uint32_t* __restrict__ keys, uint32_t* __restrict__ out,
                  uint64_t n, DevCounters* __restrict__ ctr) {
+  using G = Geo<B>;
+  extern __shared__ __align__(1024) unsigned char smem[];
   const int lane = threadIdx.x & 31;
-  const uint64_t warp = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const uint64_t n_warps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
-  const uint64_t n_batches = (n + 31) >> 5;
+  const uint32_t stage = smem_u32(smem) + (threadIdx.x >> 5) * G::WARP_BYTES;
+  const uint32_t lt_mask = (1u << lane) - 1u;
 
+  Slice sl = warp_slice(n);
+  keys += sl.start;
+  out += sl.start;
   uint32_t probes = 0, hits = 0;
   unsigned long long vsum = 0;
 
-  for (uint64_t batch = warp; batch < n_batches; batch += n_warps) {
-    const uint64_t idx = (batch << 5) + lane;
-    const bool valid = idx < n;
-    const uint32_t key = valid ? __ldcs(keys + idx) : kEmptyKey;
-    uint32_t result = kEmptyKey;
-    bool pending = valid && key != kEmptyKey;  // the sentinel is never a stored key (core.hpp:23-24)
+  bool have = false;
+  uint32_t key = 0, round = 0, idx = 0;
+  uint32_t ahead = lane < sl.len ? __ldg(keys + lane) : 0u;  // next 32 keys of the slice
 
-#pragma unroll
-    for (int i = 0; i < H; ++i) {
-      if (i > 0 && !__any_sync(kFullMask, pending)) break;
-      const uint32_t bid = bucket_index(t.h[i], key);
-      bool found, notfull;
-      uint32_t value;
-      probe_find<B>(t.store, bid, pending, key, lane, found, value, notfull);
-      if (pending) {
+  for (;;) {
+    // ---- refill: idle lanes take the next unread queries, in order
+    const uint32_t idle = __ballot_sync(kFullMask, !have);
+    if (idle != 0 && sl.cursor < sl.len) {
+      const uint32_t rank = __popc(idle & lt_mask);
+      const uint32_t fresh = __shfl_sync(kFullMask, ahead, rank);
+      if (!have && sl.cursor + rank < sl.len) {
+        key = fresh;
+        idx = sl.cursor + rank;
+        round = 0;
+        have = true;
+      }
+      sl.cursor = min(sl.cursor + __popc(idle), sl.len);
+      ahead = sl.cursor + lane < sl.len ? __ldg(keys + sl.cursor + lane) : 0u;
+    }
+    if (!__any_sync(kFullMask, have)) break;
+
+    // ---- one probe per lane
+    // the sentinel is never a stored key (core.hpp:23-24): it is answered "absent" without a probe
+    const bool probing = have && key != kEmptyKey;
+    const uint32_t bid = probing ? bucket_index_sel<H>(t, round, key) : kNoBucket;
+    fetch_issue<B>(stage, t.store, bid, lane);
+    if (G::STAGED) fetch_wait();
+    if (have) {
+      bool done = true;
+      uint32_t answer = kEmptyKey;
+      if (probing) {
+        const Scan s = scan_bucket<B, true>(stage, t.store, bid, key, lane);
         ++probes;
-        if (found) {
-          result = value;
-          pending = false;
+        if (s.found) {
+          answer = s.value;
           ++hits;
-          vsum += value;
-        } else if (EARLY_EXIT && notfull) {
-          pending = false;  // a bucket that ever evicted stays full (table.cpp:104)
+          vsum += s.value;
+        } else if ((EARLY_EXIT && s.load < B) || round == H - 1) {
+          // a bucket that ever evicted stays full (table.cpp:104); or every candidate was read
+        } else {
+          ++round;
+          done = false;
         }
       }
+      if (done) {
+        out[idx] = answer;
+        have = false;
+      }
     }
-    if (valid) __stcs(out + idx, result);
+    if (G::STAGED) __syncwarp();  // all rows scanned before the next round overwrites them
   }
 
-  const unsigned long long p = warp_sum(probes), h = warp_sum(hits), s = warp_sum(vsum);
-  if (lane == 0 && ctr != nullptr) {
-    if (p) atomicAdd(&ctr->find_probes, p);
-    if (h) atomicAdd(&ctr->find_hits, h);
-    if (s) atomicAdd(&ctr->find_value_sum, s);
+  if (ctr != nullptr) {
+    const unsigned long long p = warp_sum(probes), h = warp_sum(hits), s = warp_sum(vsum);
+    if (lane == 0) {
+      if (p) atomicAdd(&ctr->find_probes, p);
+      if (h) atomicAdd(&ctr->find_hits, h);
+      if (s) atomicAdd(&ctr->find_value_sum, s);
+    }
   }
 }
 
@@ -70,8 +98,10 @@ template <int B, int H, bool EARLY_EXIT>
 static cudaError_t launch_one(const TableView& t, const uint32_t* keys, uint32_t* out, uint64_t n, DevCounters* ctr,
                               int sm_count, cudaStream_t stream) {
   auto kernel = bulk_find_kernel<B, H, EARLY_EXIT>;
-  const int grid = persistent_grid(kernel, kFindBlock, sm_count, n, kFindBlock);
-  kernel<<<grid, kFindBlock, 0, stream>>>(t, keys, out, n, ctr);
+  constexpr int block = block_threads<B>(1);
+  constexpr int smem = (block / 32) * Geo<B>::WARP_BYTES;
+  const int grid = persistent_grid(kernel, block, smem, sm_count, n, block);
+  kernel<<<grid, block, smem, stream>>>(t, keys, out, n, ctr);
   note_launch();
   return cudaGetLastError();
 }

@@ -4,8 +4,6 @@
 
 namespace bht_b200 {
 
-constexpr int kInsertBlock = 256;
-
 // Appends a dropped key to the table's failed-key log (the GPU image of build_outcome::failed_key,
 // reference: proj/include/bht/table.hpp:115-120; a bulk insert can drop more than one).
 __device__ __forceinline__ void record_failed(DevCounters* ctr, uint32_t* failed_keys, uint64_t failed_cap, uint32_t key) {
@@ -26,6 +24,43 @@ __device__ __forceinline__ void flush_insert_counters(DevCounters* ctr, int lane
     if (p) atomicAdd(&ctr->insert_probes, p);
   }
 }
+
+// The (key, value) stream of one warp: the next 32 pairs of the warp's slice are prefetched one
+// round ahead; idle lanes take them in order.
+struct PairFeed {
+  Slice sl;
+  const uint32_t* keys;    // slice-relative
+  const uint32_t* values;
+  uint32_t ahead_k, ahead_v;
+
+  __device__ __forceinline__ void init(const uint32_t* __restrict__ k, const uint32_t* __restrict__ v, uint64_t n, int lane) {
+    sl = warp_slice(n);
+    keys = k + sl.start;
+    values = v + sl.start;
+    prefetch(lane);
+  }
+  __device__ __forceinline__ void prefetch(int lane) {
+    const bool in = sl.cursor + lane < sl.len;
+    ahead_k = in ? __ldg(keys + sl.cursor + lane) : 0u;
+    ahead_v = in ? __ldg(values + sl.cursor + lane) : 0u;
+  }
+  // Returns true for lanes that received a fresh pair.
+  __device__ __forceinline__ bool refill(bool have, int lane, uint32_t& key, uint32_t& val) {
+    const uint32_t idle = __ballot_sync(kFullMask, !have);
+    if (idle == 0 || sl.cursor >= sl.len) return false;
+    const uint32_t rank = __popc(idle & ((1u << lane) - 1u));
+    const uint32_t fk = __shfl_sync(kFullMask, ahead_k, rank);
+    const uint32_t fv = __shfl_sync(kFullMask, ahead_v, rank);
+    const bool got = !have && sl.cursor + rank < sl.len;
+    if (got) {
+      key = fk;
+      val = fv;
+    }
+    sl.cursor = min(sl.cursor + __popc(idle), sl.len);
+    prefetch(lane);
+    return got;
+  }
+};
 
 #define BHT_DISPATCH_BUCKET_SIZE(b, CALL)  \
   switch (b) {                             \

@@ -7,45 +7,65 @@
 // where the secondary is taken regardless (table.cpp:167-169).  A full choice fails the insert
 // (table.cpp:180); otherwise atomicCAS(empty -> pair) at slot = load of the choice; on a lost race
 // start over from the primary.  1 or 3 probes per attempt.
+//
+// Lane state machine with two phases: phase 0 fetches the primary; a lane whose primary is at or past
+// the threshold keeps that load and, in phase 1, fetches both secondaries (two staging rows per lane)
+// before choosing.  Lanes in different phases share the same probe rounds.
 #include "insert_common.cuh"
 
 namespace bht_b200 {
 
 template <int B>
-__global__ void __launch_bounds__(kInsertBlock)
+__global__ void __launch_bounds__(block_threads<B>(2))
 bulk_insert_iht_kernel(const __grid_constant__ TableView t, const uint32_t* __restrict__ keys,
                        const uint32_t* __restrict__ values, uint64_t n, DevCounters* __restrict__ ctr,
                        uint32_t* __restrict__ failed_keys, uint64_t failed_cap) {
+  using G = Geo<B>;
+  extern __shared__ __align__(1024) unsigned char smem[];
   const int lane = threadIdx.x & 31;
-  const uint64_t warp = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const uint64_t n_warps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
-  const uint64_t n_batches = (n + 31) >> 5;
+  const uint32_t stage0 = smem_u32(smem) + (threadIdx.x >> 5) * (2 * G::WARP_BYTES);
+  const uint32_t stage1 = stage0 + G::WARP_BYTES;
   unsigned long long* store = reinterpret_cast<unsigned long long*>(t.store);
   uint32_t n_ins = 0, n_fail = 0, n_probe = 0;
 
-  for (uint64_t batch = warp; batch < n_batches; batch += n_warps) {
-    const uint64_t idx = (batch << 5) + lane;
-    const bool valid = idx < n;
-    const uint32_t key = valid ? __ldcs(keys + idx) : kEmptyKey;
-    const uint32_t val = valid ? __ldcs(values + idx) : kEmptyKey;
-    bool pending = valid;
-    const uint32_t pb = bucket_index(t.h[0], key);
-    uint32_t retries = 0;
+  PairFeed feed;
+  feed.init(keys, values, n, lane);
+  bool have = false, overflow = false;  // overflow: phase 1 (primary already read, at or past t)
+  uint32_t key = 0, val = 0, pb = 0, pl = 0, s0 = 0, s1 = 0, retries = 0;
 
-    while (__any_sync(kFullMask, pending)) {
-      uint32_t pl;
-      probe_load<B>(t.store, pb, pending, lane, pl);
-      const bool overflow = pending && pl >= t.threshold;
-      uint32_t s0 = 0, s1 = 0, l0 = 0, l1 = 0;
-      if (__any_sync(kFullMask, overflow)) {
-        s0 = bucket_index(t.h[1], key);
-        s1 = bucket_index(t.h[2], key);
-        probe_load_pair<B>(t.store, s0, s1, overflow, lane, l0, l1);
-      }
-      if (pending) {
-        n_probe += overflow ? 3 : 1;
-        uint32_t cb = pb, cl = pl;
-        if (overflow && (t.prose || l0 != B || l1 != B)) {
+  for (;;) {
+    if (feed.refill(have, lane, key, val)) {
+      have = true;
+      overflow = false;
+      pb = bucket_index(t.h[0], key);
+      retries = 0;
+    }
+    if (!__any_sync(kFullMask, have)) break;
+
+    fetch_issue<B>(stage0, t.store, have ? (overflow ? s0 : pb) : kNoBucket, lane);
+    fetch_issue<B>(stage1, t.store, have && overflow ? s1 : kNoBucket, lane);
+    if (G::STAGED) fetch_wait();
+    if (have) {
+      bool claim = false;
+      uint32_t cb = pb, cl = 0;
+      if (!overflow) {
+        pl = scan_bucket<B, false>(stage0, t.store, pb, key, lane).load;
+        n_probe += 1;
+        if (pl >= t.threshold) {
+          overflow = true;  // secondaries next round
+          s0 = bucket_index(t.h[1], key);
+          s1 = bucket_index(t.h[2], key);
+        } else {
+          claim = true;
+          cl = pl;
+        }
+      } else {
+        const uint32_t l0 = scan_bucket<B, false>(stage0, t.store, s0, key, lane).load;
+        const uint32_t l1 = scan_bucket<B, false>(stage1, t.store, s1, key, lane).load;
+        n_probe += 2;
+        claim = true;
+        cl = pl;
+        if (t.prose || l0 != B || l1 != B) {
           if (l0 <= l1) {
             cb = s0;
             cl = l0;
@@ -54,22 +74,22 @@ bulk_insert_iht_kernel(const __grid_constant__ TableView t, const uint32_t* __re
             cl = l1;
           }
         }
+      }
+      if (claim) {
         if (cl == B || retries > t.retry_cap) {
           ++n_fail;
           record_failed(ctr, failed_keys, failed_cap, key);
-          pending = false;
+          have = false;
+        } else if (atomicCAS(store + static_cast<uint64_t>(cb) * B + cl, kEmptySlot, pack_pair(key, val)) == kEmptySlot) {
+          ++n_ins;
+          have = false;
         } else {
-          const unsigned long long old =
-              atomicCAS(store + static_cast<uint64_t>(cb) * B + cl, kEmptySlot, pack_pair(key, val));
-          if (old == kEmptySlot) {
-            ++n_ins;
-            pending = false;
-          } else {
-            ++retries;
-          }
+          ++retries;
+          overflow = false;  // lost the slot: start over from the primary
         }
       }
     }
+    if (G::STAGED) __syncwarp();
   }
   flush_insert_counters(ctr, lane, n_ins, n_fail, n_probe);
 }
@@ -79,8 +99,10 @@ static cudaError_t launch_one(const TableView& t, const uint32_t* keys, const ui
                               DevCounters* ctr, uint32_t* failed_keys, uint64_t failed_cap, int sm_count,
                               cudaStream_t stream) {
   auto kernel = bulk_insert_iht_kernel<B>;
-  const int grid = persistent_grid(kernel, kInsertBlock, sm_count, n, kInsertBlock);
-  kernel<<<grid, kInsertBlock, 0, stream>>>(t, keys, values, n, ctr, failed_keys, failed_cap);
+  constexpr int block = block_threads<B>(2);
+  constexpr int smem = (block / 32) * 2 * Geo<B>::WARP_BYTES;
+  const int grid = persistent_grid(kernel, block, smem, sm_count, n, block);
+  kernel<<<grid, block, smem, stream>>>(t, keys, values, n, ctr, failed_keys, failed_cap);
   note_launch();
   return cudaGetLastError();
 }

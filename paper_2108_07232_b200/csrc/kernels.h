@@ -8,10 +8,6 @@
 
 namespace bht_b200 {
 
-struct LaunchGeom {
-  int sm_count;
-};
-
 // find.cu — K3 bulk_find<kind, b>.  early_exit selects bcht_find's non-full early exit
 // (table.cpp:104); without it the same kernel is bp2ht_find / iht_find / bcht_find_no_early_exit.
 cudaError_t launch_find(const TableView& t, bool early_exit, const uint32_t* keys, uint32_t* out, uint64_t n,
@@ -51,11 +47,13 @@ cudaError_t launch_generate_keys(uint64_t seed, uint64_t offset, uint64_t n, uin
 void note_launch();
 uint64_t launch_count();
 
-// Persistent grid: enough CTAs of `block` threads to fill the device, never more than the work.
+// Persistent grid: enough CTAs of `block` threads (+ `smem` dynamic bytes) to fill the device, never
+// more than the work.
 template <typename Kernel>
-inline int persistent_grid(Kernel kernel, int block, int sm_count, uint64_t work_items, uint64_t items_per_block) {
+inline int persistent_grid(Kernel kernel, int block, int smem, int sm_count, uint64_t work_items,
+                           uint64_t items_per_block) {
   int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, 0) != cudaSuccess || per_sm < 1) per_sm = 1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, smem) != cudaSuccess || per_sm < 1) per_sm = 1;
   uint64_t need = (work_items + items_per_block - 1) / items_per_block;
   if (need < 1) need = 1;
   const uint64_t fill = static_cast<uint64_t>(per_sm) * static_cast<uint64_t>(sm_count);

@@ -4,17 +4,22 @@
 // bucket (= one probe, bucket.hpp:18-21), compute_load (:26-31), full (:33) and find_key_value
 // (:36-41).  cas_at_slot / exch_at_slot (:45-55) are single 64-bit atomics issued by the callers.
 //
-// Geometry.  A bucket of B 8-byte slots is read by a tile of LPB = B/2 lanes, each issuing ONE
-// 16-byte vector load (two slots), so a b=16 bucket is one fully-used 128-byte line fetched by 8
-// lanes and a warp-wide load instruction covers 4 buckets (B=1 is one 8-byte load per lane).
-// Match / load results come from __ballot_sync + __ffs / __popc over the tile's slice of the warp
-// ballot.
+// Shape of one probe round of a warp (32 keys, one per lane):
 //
-// Batching.  Every lane owns one key.  The LPB lanes of a tile serve their own LPB keys in LPB
-// steps (step u serves the key of tile lane u), and up to BATCH = 8 steps have their loads issued
-// back to back before any is consumed, so one warp keeps up to 8 x 4 = 32 independent 128-byte
-// lines in flight.  Steps in which no tile of the warp has a pending key are skipped (warp-uniform
-// branch), which keeps later probe rounds cheap.
+//   fetch   A bucket of B 8-byte slots is B/2 16-byte chunks.  A tile of C = B/2 lanes copies one
+//           bucket with ONE 16-byte cp.async (LDGSTS, L2-only) per lane straight into shared
+//           memory, so a warp-wide copy instruction moves 32/C whole buckets, every 32-byte sector
+//           it touches is fully used (128-byte aligned buckets at b = 16), and no register is tied
+//           up while the line is in flight: a warp keeps 32 buckets outstanding for the cost of
+//           C instructions, and the SM keeps (resident warps x 32) lines in flight.
+//   scan    After cp.async.wait_group + __syncwarp every lane scans ITS OWN key's bucket from
+//           shared memory with 16-byte LDS: 32 keys are matched in parallel by plain per-lane
+//           compares — no ballots, no shuffles, no serialisation over the tile.
+//
+// Shared-memory layout: one row of 16*C bytes per lane; chunk c of row r is stored at position
+// c ^ g(r), an XOR swizzle that makes both the tile-wise writes and the lane-wise reads
+// bank-conflict free (see swizzle()).  Buckets of 1 or 2 slots are a single 8/16-byte load per
+// lane and skip the staging.
 #pragma once
 #include <cuda_runtime.h>
 
@@ -25,235 +30,157 @@
 namespace bht_b200 {
 
 constexpr unsigned kFullMask = 0xFFFFFFFFu;
+constexpr uint32_t kNoBucket = 0xFFFFFFFFu;  // "this lane has no probe this round" (bucket ids are < 2^32 - 1)
 
 template <int B>
 struct Geo {
   static_assert(B == 1 || B == 2 || B == 4 || B == 8 || B == 16 || B == 32 || B == 64, "bucket size");
-  static constexpr int SPL = B >= 2 ? 2 : 1;      // slots per lane
-  static constexpr int LPB = B / SPL;             // lanes per bucket (tile width)
-  static constexpr int BATCH = LPB < 8 ? LPB : 8; // probe steps whose loads are batched
-  static constexpr int PAIR_BATCH = LPB < 4 ? LPB : 4;
-  static constexpr uint32_t GMASK = LPB == 32 ? 0xFFFFFFFFu : ((1u << LPB) - 1u);
+  static constexpr bool STAGED = B >= 4;            // fetched through shared memory
+  static constexpr int C = B >= 2 ? B / 2 : 1;      // 16-byte chunks per bucket = lanes per fetch tile
+  static constexpr int T = 32 / C;                  // buckets fetched by one warp-wide copy instruction
+  static constexpr int ROW_BYTES = B * 8;
+  static constexpr int WARP_BYTES = STAGED ? 32 * ROW_BYTES : 0;  // staging bytes per warp per probed bucket
+  // g(r): rows whose chunks share a bank group under a 16-byte access get different rotations
+  __device__ static __forceinline__ uint32_t swizzle(uint32_t row) {
+    if constexpr (C >= 8) return row & (C - 1);
+    else if constexpr (C == 4) return (row >> 1) & 3;
+    else return (row >> 2) & 1;
+  }
 };
 
-// Two adjacent slots as loaded by one lane: (k0, v0) = slot 2*sub, (k1, v1) = slot 2*sub+1.
-struct Slot2 {
-  uint32_t k0, v0, k1, v1;
-};
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
 
-__device__ __forceinline__ Slot2 empty_slot2() { return Slot2{kEmptyKey, kEmptyKey, kEmptyKey, kEmptyKey}; }
-
-// Read-only table (find): non-coherent path, no L1 allocation — every line is used exactly once.
-__device__ __forceinline__ uint4 ld_table_nc_v4(const void* p) {
+// 16-byte global -> shared copy that bypasses L1 (coherent at L2: sees other SMs' atomics).
+// src_bytes = 16 copies, src_bytes = 0 zero-fills the destination without touching global memory, so
+// lanes without a probe stay on the same branch-free instruction stream.
+__device__ __forceinline__ void cp_async_16(uint32_t smem_dst, uint64_t gmem_src, uint32_t src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_dst), "l"(gmem_src), "r"(src_bytes) : "memory");
+}
+// a * b + c with a 32-bit a, b and a 64-bit c: one IMAD.WIDE
+__device__ __forceinline__ uint64_t mad_wide(uint32_t a, uint32_t b, uint64_t c) {
+  uint64_t d;
+  asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(d) : "r"(a), "r"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+}
+__device__ __forceinline__ uint4 lds_v4(uint32_t addr) {
   uint4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-               : "l"(p));
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "r"(addr));
   return r;
 }
-__device__ __forceinline__ uint2 ld_table_nc_v2(const void* p) {
-  uint2 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
+__device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
+  uint32_t r;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(r) : "r"(addr));
   return r;
 }
-// Table under construction (insert): L2-coherent loads; L1 may hold stale lines across SMs.
-__device__ __forceinline__ uint4 ld_table_cg_v4(const void* p) {
+__device__ __forceinline__ uint4 ldg_cg_v4(const void* p) {
   uint4 r;
-  asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-               : "l"(p)
-               : "memory");
+  asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p) : "memory");
   return r;
 }
-__device__ __forceinline__ uint2 ld_table_cg_v2(const void* p) {
+__device__ __forceinline__ uint2 ldg_cg_v2(const void* p) {
   uint2 r;
   asm volatile("ld.global.cg.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p) : "memory");
   return r;
 }
 
-// One lane's share of bucket `bid`: slots [SPL*sub, SPL*sub + SPL).
-template <int B, bool COHERENT>
-__device__ __forceinline__ Slot2 load_lane(const uint64_t* __restrict__ store, uint32_t bid, int sub) {
-  const uint64_t* p = store + static_cast<uint64_t>(bid) * B + sub * Geo<B>::SPL;
-  if constexpr (B >= 2) {
-    const uint4 v = COHERENT ? ld_table_cg_v4(p) : ld_table_nc_v4(p);
-    return Slot2{v.x, v.y, v.z, v.w};
-  } else {
-    const uint2 v = COHERENT ? ld_table_cg_v2(p) : ld_table_nc_v2(p);
-    return Slot2{v.x, v.y, kEmptyKey, kEmptyKey};
-  }
-}
+// Result of scanning one bucket for one key.
+struct Scan {
+  uint32_t load;   // occupied slots (compute_load, bucket.hpp:26-31); with WANT_KEY only B (full) or 0 (not full)
+  uint32_t value;  // value of the lowest slot holding the key (find_key_value, bucket.hpp:36-41)
+  bool found;
+};
 
-// OR of the per-tile activity masks: bit u set <=> some tile of the warp has a pending key at tile
-// lane u.  Warp-uniform.
-template <int LPB>
-__device__ __forceinline__ uint32_t union_over_tiles(uint32_t act) {
-#pragma unroll
-  for (int s = LPB; s < 32; s <<= 1) act |= act >> s;
-  return act;
-}
-
-// ---- find probe -----------------------------------------------------------------------------
-// For every lane with my_active: one probe of bucket my_bid looking for my_key.
-//   found   <=> some slot holds my_key (lowest slot wins, bucket.hpp:36-41)
-//   value   value of that slot
-//   notfull <=> the bucket has an empty slot (!full(), bucket.hpp:33)
+// ---- fetch ------------------------------------------------------------------------------------
+// Every lane names the bucket it wants (my_bid, or kNoBucket).  Staged sizes: the warp copies all
+// named buckets into `stage` (shared address of this warp's 32 rows).  Call fetch_wait() before
+// scanning, and __syncwarp() after scanning before the rows are fetched into again.
 template <int B>
-__device__ __forceinline__ void probe_find(const uint64_t* __restrict__ store, uint32_t my_bid, bool my_active,
-                                           uint32_t my_key, int lane, bool& found, uint32_t& value, bool& notfull) {
+__device__ __forceinline__ void fetch_issue(uint32_t stage, const uint64_t* __restrict__ store, uint32_t my_bid, int lane) {
   using G = Geo<B>;
-  found = false;
-  notfull = false;
-  value = kEmptyKey;
-  if constexpr (G::LPB == 1) {
-    if (my_active) {
-      const Slot2 s = load_lane<B, false>(store, my_bid, 0);
-      const bool m0 = s.k0 == my_key;
-      const bool m1 = B == 2 && s.k1 == my_key;
-      found = m0 || m1;
-      value = m0 ? s.v0 : (m1 ? s.v1 : kEmptyKey);
-      notfull = s.k0 == kEmptyKey || (B == 2 && s.k1 == kEmptyKey);
-    }
-  } else {
-    const int sub = lane & (G::LPB - 1);
-    const int gbase = lane & ~(G::LPB - 1);
-    const uint32_t act = __ballot_sync(kFullMask, my_active);
-    const uint32_t any = union_over_tiles<G::LPB>(act);
-    const uint32_t mine = (act >> gbase) & G::GMASK;
+  if constexpr (G::STAGED) {
+    const uint32_t sub = lane & (G::C - 1);
+    const uint32_t t = lane / G::C;
+    if (!__any_sync(kFullMask, my_bid != kNoBucket)) return;  // warp-uniform: nobody probes (iht second row)
+    const uint64_t lane_src = reinterpret_cast<uint64_t>(store) + sub * 16;
 #pragma unroll
-    for (int base = 0; base < G::LPB; base += G::BATCH) {
-      Slot2 s[G::BATCH];
-#pragma unroll
-      for (int u = 0; u < G::BATCH; ++u) {
-        if (!((any >> (base + u)) & 1u)) continue;  // warp-uniform
-        const uint32_t bid = __shfl_sync(kFullMask, my_bid, base + u, G::LPB);
-        s[u] = ((mine >> (base + u)) & 1u) ? load_lane<B, false>(store, bid, sub) : empty_slot2();
-      }
-#pragma unroll
-      for (int u = 0; u < G::BATCH; ++u) {
-        if (!((any >> (base + u)) & 1u)) continue;
-        const uint32_t qk = __shfl_sync(kFullMask, my_key, base + u, G::LPB);
-        const bool a = (mine >> (base + u)) & 1u;
-        const bool m0 = a && s[u].k0 == qk;
-        const bool m1 = a && s[u].k1 == qk;
-        const uint32_t bm = __ballot_sync(kFullMask, m0 || m1);
-        const uint32_t be = __ballot_sync(kFullMask, s[u].k0 == kEmptyKey || s[u].k1 == kEmptyKey);
-        const uint32_t gm = (bm >> gbase) & G::GMASK;
-        const uint32_t myval = m0 ? s[u].v0 : s[u].v1;
-        const int src = gm ? (__ffs(gm) - 1) : 0;
-        const uint32_t val = __shfl_sync(kFullMask, myval, src, G::LPB);
-        if (sub == base + u) {
-          found = gm != 0;
-          value = gm ? val : kEmptyKey;
-          notfull = ((be >> gbase) & G::GMASK) != 0;
-        }
-      }
+    for (int u = 0; u < G::C; ++u) {
+      const uint32_t row = u * G::T + t;
+      const uint32_t bid = __shfl_sync(kFullMask, my_bid, row);
+      const bool on = bid != kNoBucket;
+      const uint32_t dst = stage + row * G::ROW_BYTES + ((sub ^ G::swizzle(row)) << 4);
+      cp_async_16(dst, mad_wide(on ? bid : 0u, G::ROW_BYTES, lane_src), on ? 16u : 0u);
     }
   }
 }
 
-// ---- load probe (insert side) ---------------------------------------------------------------
-// For every lane with my_active: load = number of occupied slots of bucket my_bid
-// (compute_load, bucket.hpp:26-31), read through L2 so concurrent inserts are visible.
-template <int B>
-__device__ __forceinline__ void probe_load(const uint64_t* __restrict__ store, uint32_t my_bid, bool my_active,
-                                           int lane, uint32_t& load) {
-  using G = Geo<B>;
-  load = 0;
-  if constexpr (G::LPB == 1) {
-    if (my_active) {
-      const Slot2 s = load_lane<B, true>(store, my_bid, 0);
-      load = (s.k0 != kEmptyKey) + (B == 2 && s.k1 != kEmptyKey);
-    }
-  } else {
-    const int sub = lane & (G::LPB - 1);
-    const int gbase = lane & ~(G::LPB - 1);
-    const uint32_t act = __ballot_sync(kFullMask, my_active);
-    const uint32_t any = union_over_tiles<G::LPB>(act);
-    const uint32_t mine = (act >> gbase) & G::GMASK;
-#pragma unroll
-    for (int base = 0; base < G::LPB; base += G::BATCH) {
-      Slot2 s[G::BATCH];
-#pragma unroll
-      for (int u = 0; u < G::BATCH; ++u) {
-        if (!((any >> (base + u)) & 1u)) continue;
-        const uint32_t bid = __shfl_sync(kFullMask, my_bid, base + u, G::LPB);
-        s[u] = ((mine >> (base + u)) & 1u) ? load_lane<B, true>(store, bid, sub) : empty_slot2();
-      }
-#pragma unroll
-      for (int u = 0; u < G::BATCH; ++u) {
-        if (!((any >> (base + u)) & 1u)) continue;
-        const uint32_t n0 = __ballot_sync(kFullMask, s[u].k0 != kEmptyKey);
-        const uint32_t n1 = __ballot_sync(kFullMask, s[u].k1 != kEmptyKey);
-        if (sub == base + u) load = __popc((n0 >> gbase) & G::GMASK) + __popc((n1 >> gbase) & G::GMASK);
-      }
-    }
-  }
+__device__ __forceinline__ void fetch_wait() {
+  cp_async_wait_all();
+  __syncwarp();
 }
 
-// Two buckets per key (bp2ht both choices, iht both secondaries): loads of bid_a and bid_b.
-template <int B>
-__device__ __forceinline__ void probe_load_pair(const uint64_t* __restrict__ store, uint32_t bid_a, uint32_t bid_b,
-                                                bool my_active, int lane, uint32_t& load_a, uint32_t& load_b) {
+// ---- scan -------------------------------------------------------------------------------------
+// The lane's own bucket: staged sizes read row `lane` of `stage`; b <= 2 loads straight from
+// global memory through L2.  WANT_KEY = false skips the key match (insert needs the load only).
+template <int B, bool WANT_KEY>
+__device__ __forceinline__ Scan scan_bucket(uint32_t stage, const uint64_t* __restrict__ store, uint32_t bid, uint32_t key,
+                                            int lane) {
   using G = Geo<B>;
-  load_a = 0;
-  load_b = 0;
-  if constexpr (G::LPB == 1) {
-    if (my_active) {
-      const Slot2 a = load_lane<B, true>(store, bid_a, 0);
-      const Slot2 b = load_lane<B, true>(store, bid_b, 0);
-      load_a = (a.k0 != kEmptyKey) + (B == 2 && a.k1 != kEmptyKey);
-      load_b = (b.k0 != kEmptyKey) + (B == 2 && b.k1 != kEmptyKey);
-    }
-  } else {
-    const int sub = lane & (G::LPB - 1);
-    const int gbase = lane & ~(G::LPB - 1);
-    const uint32_t act = __ballot_sync(kFullMask, my_active);
-    const uint32_t any = union_over_tiles<G::LPB>(act);
-    const uint32_t mine = (act >> gbase) & G::GMASK;
-#pragma unroll
-    for (int base = 0; base < G::LPB; base += G::PAIR_BATCH) {
-      Slot2 sa[G::PAIR_BATCH], sb[G::PAIR_BATCH];
-#pragma unroll
-      for (int u = 0; u < G::PAIR_BATCH; ++u) {
-        if (!((any >> (base + u)) & 1u)) continue;
-        const uint32_t ba = __shfl_sync(kFullMask, bid_a, base + u, G::LPB);
-        const uint32_t bb = __shfl_sync(kFullMask, bid_b, base + u, G::LPB);
-        const bool a = (mine >> (base + u)) & 1u;
-        sa[u] = a ? load_lane<B, true>(store, ba, sub) : empty_slot2();
-        sb[u] = a ? load_lane<B, true>(store, bb, sub) : empty_slot2();
+  Scan r;
+  r.load = 0;
+  r.value = kEmptyKey;
+  r.found = false;
+  if constexpr (!G::STAGED) {
+    if constexpr (B == 1) {
+      const uint2 s = ldg_cg_v2(store + bid);
+      r.load = s.x != kEmptyKey;
+      if (WANT_KEY && s.x == key) {
+        r.found = true;
+        r.value = s.y;
       }
-#pragma unroll
-      for (int u = 0; u < G::PAIR_BATCH; ++u) {
-        if (!((any >> (base + u)) & 1u)) continue;
-        const uint32_t a0 = __ballot_sync(kFullMask, sa[u].k0 != kEmptyKey);
-        const uint32_t a1 = __ballot_sync(kFullMask, sa[u].k1 != kEmptyKey);
-        const uint32_t b0 = __ballot_sync(kFullMask, sb[u].k0 != kEmptyKey);
-        const uint32_t b1 = __ballot_sync(kFullMask, sb[u].k1 != kEmptyKey);
-        if (sub == base + u) {
-          load_a = __popc((a0 >> gbase) & G::GMASK) + __popc((a1 >> gbase) & G::GMASK);
-          load_b = __popc((b0 >> gbase) & G::GMASK) + __popc((b1 >> gbase) & G::GMASK);
-        }
+    } else {
+      const uint4 s = ldg_cg_v4(store + static_cast<uint64_t>(bid) * 2);
+      r.load = (s.x != kEmptyKey) + (s.z != kEmptyKey);
+      if (WANT_KEY) {
+        if (s.z == key) { r.found = true; r.value = s.w; }
+        if (s.x == key) { r.found = true; r.value = s.y; }  // lowest slot wins
       }
     }
-  }
-}
-
-// Tile-synchronous probe: all LPB lanes of a tile pass the same bid / have; returns the load of
-// that one bucket to every lane of the tile (used by the eviction state machine).
-template <int B>
-__device__ __forceinline__ uint32_t tile_probe_load(const uint64_t* __restrict__ store, uint32_t bid, bool have, int lane) {
-  using G = Geo<B>;
-  const int sub = lane & (G::LPB - 1);
-  const Slot2 s = have ? load_lane<B, true>(store, bid, sub) : empty_slot2();
-  if constexpr (G::LPB == 1) {
-    return (s.k0 != kEmptyKey) + (B == 2 && s.k1 != kEmptyKey);
   } else {
-    const int gbase = lane & ~(G::LPB - 1);
-    const uint32_t n0 = __ballot_sync(kFullMask, s.k0 != kEmptyKey);
-    const uint32_t n1 = __ballot_sync(kFullMask, s.k1 != kEmptyKey);
-    return __popc((n0 >> gbase) & G::GMASK) + __popc((n1 >> gbase) & G::GMASK);
+    const uint32_t row = stage + lane * G::ROW_BYTES;
+    const uint32_t base = row + (G::swizzle(lane) << 4);  // row is ROW_BYTES-aligned: XOR below stays inside it
+    if constexpr (WANT_KEY) {
+      // find: value of the lowest matching slot + "has an empty slot" (0xFFFFFFFF is the largest key)
+      uint32_t top = 0, value = kEmptyKey;
+#pragma unroll
+      for (int c = G::C - 1; c >= 0; --c) {  // descending, so the lowest matching slot is the one kept
+        const uint4 s = lds_v4(base ^ (c << 4));
+        top = max(top, max(s.x, s.z));
+        value = s.z == key ? s.w : value;
+        value = s.x == key ? s.y : value;
+      }
+      // stored values never equal the sentinel (core.hpp:20-24), so it doubles as "no match"
+      r.value = value;
+      r.found = value != kEmptyKey;
+      r.load = top == kEmptyKey ? 0u : static_cast<uint32_t>(B);  // only full / not full is reported
+    } else {
+      // insert: the load is the index of the first empty slot.  Slots are only ever claimed at index
+      // = load (table.cpp:85) and full buckets never drain, so the occupied slots of a bucket are a
+      // prefix and compute_load's popcount (bucket.hpp:26-31) equals this binary search: log2(B)+1
+      // 4-byte reads instead of B.
+      auto key_at = [&](uint32_t i) { return lds_u32((base ^ ((i >> 1) << 4)) + ((i & 1u) << 3)); };
+      uint32_t pos = 0;
+#pragma unroll
+      for (int step = B / 2; step >= 1; step >>= 1) {
+        if (key_at(pos + step - 1) != kEmptyKey) pos += step;
+      }
+      if (key_at(pos) != kEmptyKey) pos += 1;
+      r.load = pos;
+    }
   }
+  return r;
 }
 
 // ---- shared kernel plumbing -----------------------------------------------------------------
@@ -270,6 +197,18 @@ struct TableView {
   uint32_t prose;
   uint32_t retry_cap;  // bound on CAS-loss retries per key (a legit table needs <= 3*b)
 };
+
+// h_i(key) with a per-lane i: the constants are picked with selects (a divergent constant-bank
+// index would serialise).
+template <int H>
+__device__ __forceinline__ uint32_t bucket_index_sel(const TableView& t, uint32_t i, uint32_t key) {
+  HashFn h = t.h[0];
+#pragma unroll
+  for (int j = 1; j < H; ++j) {
+    if (i == static_cast<uint32_t>(j)) h = t.h[j];
+  }
+  return bucket_index(h, key);
+}
 
 struct DevCounters {
   // ---- per call: zeroed at the start of every bht_insert / bht_find ----
@@ -296,6 +235,37 @@ __device__ __forceinline__ unsigned long long warp_sum(unsigned long long v) {
 
 __device__ __forceinline__ uint64_t pack_pair(uint32_t key, uint32_t value) {
   return (static_cast<uint64_t>(value) << 32) | key;
+}
+
+// ---- work distribution ------------------------------------------------------------------------
+// Every warp owns one contiguous slice of the input and streams through it as a lane-level state
+// machine: a lane that has finished its key takes the next unread key of the slice, so every probe
+// round is dense (32 probes per warp) no matter how many rounds individual keys need.  The next 32
+// keys of the slice are prefetched one round ahead and handed out with a shuffle.
+struct Slice {
+  uint64_t start;        // first element of the warp's slice
+  uint32_t len, cursor;  // slice length and next unread element, relative to start
+};
+
+__device__ __forceinline__ Slice warp_slice(uint64_t n) {
+  const uint64_t warp = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t n_warps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+  uint64_t len = (n + n_warps - 1) / n_warps;
+  len = (len + 31) & ~31ull;  // whole 128-byte lines of keys per warp
+  Slice s;
+  s.start = warp * len < n ? warp * len : n;
+  s.len = static_cast<uint32_t>(s.start + len < n ? len : n - s.start);
+  s.cursor = 0;
+  return s;
+}
+
+// Threads per block for a kernel that stages `rows_per_lane` buckets of B slots per lane: keeps the
+// staging area of a block at or below 32 KiB so that several blocks share an SM.
+template <int B>
+constexpr int block_threads(int rows_per_lane) {
+  int t = 256;
+  while (t > 32 && (t / 32) * Geo<B>::WARP_BYTES * rows_per_lane > 32 * 1024) t /= 2;
+  return t;
 }
 
 }  // namespace bht_b200
