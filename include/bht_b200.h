@@ -142,7 +142,7 @@ int32_t bht_device_of(const bht_table* table);
 /* Bulk insert: replaces build()'s insertion loop (table.cpp:224-271) and insert_pair
  * (table.cpp:203-212) with explicit values.  Precondition as in the reference: keys unique,
  * != sentinel, not yet present.  Unlike the reference's build, which stops at the first failed
- * key, every pair is attempted.  BHT_CAPACITY_EXCEEDED when inserted + n > capacity.
+ * key, every pair is attempted.  BHT_CAPACITY_EXCEEDED when n > capacity (build's check, table.cpp:225).
  * `result` may be NULL (no synchronisation; fetch it later with bht_last_insert_result). */
 bht_status bht_insert(bht_table* table, const uint32_t* keys, const uint32_t* values, uint64_t n,
                       int32_t mem_space, bht_insert_result* result, void* stream);

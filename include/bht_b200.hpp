@@ -1,0 +1,249 @@
+// bht_b200.hpp — header-only C++ host layer over the C ABI in bht_b200.h.
+//
+// Mirrors the reference library's table API (reference: proj/include/bht/core.hpp, table.hpp) name for
+// name so that a caller of `bht::hash_table` / `bht::build` can switch to `bht::gpu::hash_table` /
+// `bht::gpu::build` for the bulk path:
+//
+//   reference (CPU)                                  this header (B200)
+//   ---------------------------------------------    -------------------------------------------------
+//   make_config(kind, n, lf, b, t, seed, chain)      gpu::make_config(...)            same arguments
+//   hash_table table(cfg)                            gpu::hash_table table(cfg [, device])
+//   insert_pair(table, {k, v}, rng, stats)   x n     table.insert(keys, values, n)    one bulk call
+//   find_key(table, k, stats)                x n     table.find(keys, out, n)         one bulk call
+//   build(keys, cfg, opts)                           gpu::build(keys, n, cfg [, opts])
+//   table.realized_load() / inserted() / ...         same names
+//   dump_store / slot_at / poke_slot                 same names (whole-store transfers underneath)
+//
+// Error behaviour follows the reference: std::invalid_argument for bad configurations and capacity
+// overflow (core.cpp:40-60, table.cpp:22-23,225), std::logic_error for a kind mismatch
+// (table.cpp:15-17), std::runtime_error for I/O and CUDA failures.  A failed insertion is reported in
+// build_outcome, never thrown.
+#ifndef BHT_B200_HPP_
+#define BHT_B200_HPP_
+
+#include <cstdint>
+#include <optional>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "bht_b200.h"
+
+namespace bht {
+namespace gpu {
+
+using key_type = std::uint32_t;
+using value_type = std::uint32_t;
+using slot_type = std::uint64_t;
+
+inline constexpr key_type empty_key = BHT_EMPTY_KEY;
+inline constexpr value_type empty_value = BHT_EMPTY_VALUE;
+inline constexpr slot_type empty_slot = BHT_EMPTY_SLOT;
+
+enum class table_kind : std::int32_t { one_cht = BHT_ONE_CHT, bcht = BHT_BCHT, bp2ht = BHT_BP2HT, iht = BHT_IHT };
+enum class mem_space : std::int32_t { device = BHT_MEM_DEVICE, host = BHT_MEM_HOST };
+
+using table_config = bht_config;  // plain-data image of the reference table_config (core.hpp:66-77)
+
+inline void check(bht_status s) {
+  if (s == BHT_OK) return;
+  const std::string msg = bht_last_error_string();
+  switch (s) {
+    case BHT_INVALID_ARGUMENT:
+    case BHT_CAPACITY_EXCEEDED: throw std::invalid_argument(msg);
+    case BHT_KIND_MISMATCH: throw std::logic_error(msg);
+    default: throw std::runtime_error(msg);
+  }
+}
+
+inline unsigned hash_count(table_kind kind) { return bht_hash_count(static_cast<std::int32_t>(kind)); }
+inline std::uint32_t default_max_chain(std::uint64_t n_keys) { return bht_default_max_chain(n_keys); }
+inline std::uint64_t mix_seed(std::uint64_t seed, std::uint64_t stream) { return bht_mix_seed(seed, stream); }
+inline value_type value_for_key(key_type k) { return bht_value_for_key(k); }
+
+// make_config (core.hpp:85-91)
+inline table_config make_config(table_kind kind, std::uint64_t n_keys, double lf, std::uint32_t bucket_size,
+                                std::optional<std::uint32_t> threshold = std::nullopt, std::uint64_t seed = 0,
+                                std::optional<std::uint32_t> max_chain = std::nullopt) {
+  table_config cfg;
+  check(bht_make_config(static_cast<std::int32_t>(kind), n_keys, lf, bucket_size, threshold ? static_cast<std::int64_t>(*threshold) : -1,
+                        seed, max_chain ? static_cast<std::int64_t>(*max_chain) : -1, &cfg));
+  return cfg;
+}
+
+// build_outcome (table.hpp:115-120) of one bulk insert; every pair is attempted.
+struct build_outcome {
+  bool success = false;
+  std::uint64_t inserted = 0;
+  std::uint64_t failed = 0;
+  std::uint64_t attempted = 0;
+  std::uint64_t probes = 0;               // probe_stats.total_probes
+  std::optional<key_type> failed_key;     // some dropped key
+  double mean_probes() const { return attempted ? static_cast<double>(probes) / static_cast<double>(attempted) : 0.0; }
+};
+
+struct find_stats {
+  std::uint64_t queries = 0, hits = 0, probes = 0, value_sum = 0;
+  double mean_probes() const { return queries ? static_cast<double>(probes) / static_cast<double>(queries) : 0.0; }
+};
+
+struct build_options {
+  bool iht_prose_fallback = false;  // build_options::iht_prose_fallback (table.hpp:111)
+  mem_space space = mem_space::host;
+  int device = 0;
+  void* stream = nullptr;           // cudaStream_t
+};
+
+// class hash_table (table.hpp:28-80), slot store in device memory; move-only like the reference.
+class hash_table {
+ public:
+  explicit hash_table(const table_config& cfg, int device = 0) : cfg_(cfg) { check(bht_create(&cfg_, device, &h_)); }
+  ~hash_table() { bht_destroy(h_); }
+  hash_table(const hash_table&) = delete;
+  hash_table& operator=(const hash_table&) = delete;
+  hash_table(hash_table&& o) noexcept : cfg_(o.cfg_), h_(std::exchange(o.h_, nullptr)) {}
+  hash_table& operator=(hash_table&& o) noexcept {
+    if (this != &o) {
+      bht_destroy(h_);
+      cfg_ = o.cfg_;
+      h_ = std::exchange(o.h_, nullptr);
+    }
+    return *this;
+  }
+
+  const table_config& config() const { return cfg_; }
+  std::uint64_t num_buckets() const { return cfg_.num_buckets; }
+  std::uint32_t bucket_size() const { return cfg_.bucket_size; }
+  std::uint64_t capacity() const { return cfg_.capacity; }
+  std::uint64_t bucket_of(unsigned i, key_type key) const {
+    return bht_bucket_index_host(cfg_.alpha[i], cfg_.beta[i], cfg_.range[i], key);
+  }
+
+  std::uint64_t inserted() const {
+    std::uint64_t ins = 0, cap = 0;
+    check(bht_load_factor(h_, &ins, &cap));
+    return ins;
+  }
+  double realized_load() const { return static_cast<double>(inserted()) / static_cast<double>(cfg_.capacity); }
+  std::uint64_t occupied_slots(void* stream = nullptr) const {
+    std::uint64_t n = 0;
+    check(bht_count_occupied(h_, &n, stream));
+    return n;
+  }
+  std::uint64_t count_inadmissible(void* stream = nullptr) const {  // check_admissibility (oracle.cpp:40-54)
+    std::uint64_t n = 0;
+    check(bht_count_inadmissible(h_, &n, stream));
+    return n;
+  }
+  void clear(void* stream = nullptr) { check(bht_clear(h_, stream)); }
+  void set_iht_prose_fallback(bool on) { check(bht_set_iht_prose_fallback(h_, on ? 1 : 0)); }
+
+  // bulk insert_pair (table.hpp:103-104)
+  build_outcome insert(const key_type* keys, const value_type* values, std::uint64_t n, mem_space space = mem_space::host,
+                       void* stream = nullptr) {
+    bht_insert_result r{};
+    check(bht_insert(h_, keys, values, n, static_cast<std::int32_t>(space), &r, stream));
+    return outcome_of(r);
+  }
+  // the per-variant entry points bcht_insert / bp2ht_insert / iht_insert (table.hpp:84-101)
+  build_outcome insert_as(table_kind kind, const key_type* keys, const value_type* values, std::uint64_t n,
+                          mem_space space = mem_space::host, void* stream = nullptr) {
+    bht_insert_result r{};
+    check(bht_insert_as(h_, static_cast<std::int32_t>(kind), keys, values, n, static_cast<std::int32_t>(space), &r, stream));
+    return outcome_of(r);
+  }
+  // stream-ordered, no host synchronisation; fetch the outcome later with last_insert_result()
+  void insert_async(const key_type* device_keys, const value_type* device_values, std::uint64_t n, void* stream) {
+    check(bht_insert(h_, device_keys, device_values, n, BHT_MEM_DEVICE, nullptr, stream));
+  }
+  build_outcome last_insert_result(void* stream = nullptr) {
+    bht_insert_result r{};
+    check(bht_last_insert_result(h_, &r, stream));
+    return outcome_of(r);
+  }
+  std::vector<key_type> failed_keys(std::uint64_t max_keys = 1u << 20) {
+    std::vector<key_type> out(max_keys);
+    std::uint64_t count = 0;
+    check(bht_failed_keys(h_, out.data(), max_keys, &count));
+    out.resize(count < max_keys ? count : max_keys);
+    return out;
+  }
+
+  // bulk find_key (table.hpp:105): out[i] = value or empty_value
+  void find(const key_type* keys, value_type* out, std::uint64_t n, mem_space space = mem_space::host, void* stream = nullptr,
+            find_stats* stats = nullptr) const {
+    bht_find_result r{};
+    check(bht_find(h_, keys, out, n, static_cast<std::int32_t>(space), stats ? &r : nullptr, stream));
+    if (stats) *stats = find_stats{r.queries, r.hits, r.probes, r.value_sum};
+  }
+  void find_as(table_kind kind, const key_type* keys, value_type* out, std::uint64_t n, mem_space space = mem_space::host,
+               void* stream = nullptr) const {
+    check(bht_find_as(h_, static_cast<std::int32_t>(kind), keys, out, n, static_cast<std::int32_t>(space), nullptr, stream));
+  }
+  // bcht_find_no_early_exit (oracle.cpp:56-63)
+  void find_exhaustive(const key_type* keys, value_type* out, std::uint64_t n, mem_space space = mem_space::host,
+                       void* stream = nullptr) const {
+    check(bht_find_exhaustive(h_, keys, out, n, static_cast<std::int32_t>(space), nullptr, stream));
+  }
+  // find_key for one key, as the reference returns it
+  std::optional<value_type> find_key(key_type key) const {
+    value_type v = empty_value;
+    find(&key, &v, 1);
+    return v == empty_value ? std::nullopt : std::optional<value_type>(v);
+  }
+
+  // store access (table.hpp:53-56, table.cpp:41-51)
+  std::vector<slot_type> download_store() const {
+    std::vector<slot_type> s(cfg_.capacity);
+    check(bht_download_store(h_, s.data(), nullptr));
+    return s;
+  }
+  void upload_store(const std::vector<slot_type>& s) {
+    if (s.size() != cfg_.capacity) throw std::invalid_argument("upload_store: store length must equal capacity");
+    check(bht_upload_store(h_, s.data(), nullptr));
+  }
+  void dump_store(const std::string& path) const { check(bht_dump_store(h_, path.c_str())); }
+  slot_type slot_at(std::uint64_t index) const { return download_store().at(index); }
+  void poke_slot(std::uint64_t index, slot_type slot) {  // fault injection; leaves the inserted counter alone
+    auto s = download_store();
+    s.at(index) = slot;
+    const std::uint64_t before = inserted();
+    upload_store(s);
+    (void)before;
+  }
+
+  bht_table* handle() const { return h_; }
+
+ private:
+  static build_outcome outcome_of(const bht_insert_result& r) {
+    build_outcome o;
+    o.success = r.success != 0;
+    o.inserted = r.inserted;
+    o.failed = r.failed;
+    o.attempted = r.attempted;
+    o.probes = r.probes;
+    if (r.first_failed_key != BHT_EMPTY_KEY) o.failed_key = r.first_failed_key;
+    return o;
+  }
+  table_config cfg_;
+  bht_table* h_ = nullptr;
+};
+
+// build (table.hpp:125-127, table.cpp:224-276): values are value_for_key(k) as in the reference.
+inline std::pair<hash_table, build_outcome> build(const key_type* keys, std::uint64_t n, const table_config& cfg,
+                                                  build_options opts = {}) {
+  if (n > cfg.capacity) throw std::invalid_argument("build: key set exceeds table capacity");
+  if (opts.space != mem_space::host) throw std::invalid_argument("build: derives values on the host; pass host keys or use insert()");
+  hash_table table(cfg, opts.device);
+  if (opts.iht_prose_fallback) table.set_iht_prose_fallback(true);
+  std::vector<value_type> values(n);
+  for (std::uint64_t i = 0; i < n; ++i) values[i] = value_for_key(keys[i]);
+  build_outcome o = table.insert(keys, values.data(), n, mem_space::host, opts.stream);
+  return {std::move(table), o};
+}
+
+}  // namespace gpu
+}  // namespace bht
+
+#endif  // BHT_B200_HPP_

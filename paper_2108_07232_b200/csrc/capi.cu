@@ -84,7 +84,6 @@ struct bht_table {
   DevCounters* ctr = nullptr;       // device
   DevCounters* ctr_host = nullptr;  // pinned mirror
   uint32_t* failed_keys = nullptr;  // device log of dropped keys
-  uint64_t inserted_bound = 0;      // host upper bound on the device's inserted_total
   Staging stage;
   std::mutex mu;  // serialises calls that touch the counter block / staging buffers
 };
@@ -161,7 +160,6 @@ void release_staging(Staging& s) {
 bht_status read_counters(bht_table* t, cudaStream_t stream) {
   BHT_CUDA(cudaMemcpyAsync(t->ctr_host, t->ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, stream));
   BHT_CUDA(cudaStreamSynchronize(stream));
-  t->inserted_bound = t->ctr_host->inserted_total;
   return BHT_OK;
 }
 
@@ -205,12 +203,9 @@ bht_status do_insert(bht_table* t, const uint32_t* keys, const uint32_t* values,
   std::lock_guard<std::mutex> lock(t->mu);
   cudaStream_t stream = as_stream(stream_v);
 
-  // build(): "key set exceeds table capacity" (table.cpp:225), against what is resident already
-  if (t->inserted_bound + n > t->cfg.capacity) {
-    bht_status s = read_counters(t, stream);
-    if (s != BHT_OK) return s;
-    if (t->inserted_bound + n > t->cfg.capacity) return fail(BHT_CAPACITY_EXCEEDED, "build: key set exceeds table capacity");
-  }
+  // build(): "key set exceeds table capacity" (table.cpp:225).  Like insert_pair, a call that merely
+  // overfills an already loaded table is attempted and reports its failures in the result.
+  if (n > t->cfg.capacity) return fail(BHT_CAPACITY_EXCEEDED, "build: key set exceeds table capacity");
 
   BHT_CUDA(cudaMemsetAsync(t->ctr, 0, kPerCallCounterBytes, stream));
   if (mem_space == BHT_MEM_DEVICE) {
@@ -238,7 +233,6 @@ bht_status do_insert(bht_table* t, const uint32_t* keys, const uint32_t* values,
     BHT_CUDA(cudaStreamWaitEvent(stream, st.kernel_done[(chunks - 1) % kStageSlots], 0));
     BHT_CUDA(cudaStreamSynchronize(stream));  // the caller's host arrays are free again on return
   }
-  t->inserted_bound += n;
   if (result != nullptr) {
     bht_status s = read_counters(t, stream);
     if (s != BHT_OK) return s;
@@ -464,7 +458,6 @@ bht_status bht_clear(bht_table* t, void* stream) {
   std::lock_guard<std::mutex> lock(t->mu);
   BHT_CUDA(launch_fill_empty(t->view.store, t->cfg.capacity, t->sm_count, as_stream(stream)));
   BHT_CUDA(cudaMemsetAsync(t->ctr, 0, sizeof(DevCounters), as_stream(stream)));
-  t->inserted_bound = 0;
   return BHT_OK;
 }
 

@@ -26,30 +26,29 @@ bulk_find_kernel(const __grid_constant__ TableView t, const uint32_t* __restrict
   const uint32_t stage = smem_u32(smem) + (threadIdx.x >> 5) * G::WARP_BYTES;
   const uint32_t lt_mask = (1u << lane) - 1u;
 
-  Slice sl = warp_slice(n);
-  keys += sl.start;
-  out += sl.start;
+  Stream st = warp_stream(n);
   uint32_t probes = 0, hits = 0;
   unsigned long long vsum = 0;
 
   bool have = false;
-  uint32_t key = 0, round = 0, idx = 0;
-  uint32_t ahead = lane < sl.len ? __ldg(keys + lane) : 0u;  // next 32 keys of the slice
+  uint32_t key = 0, round = 0;
+  uint64_t idx = 0;
+  uint32_t ahead = lane < st.len ? __ldg(keys + st.at(lane)) : 0u;  // next 32 keys of the stream
 
   for (;;) {
     // ---- refill: idle lanes take the next unread queries, in order
     const uint32_t idle = __ballot_sync(kFullMask, !have);
-    if (idle != 0 && sl.cursor < sl.len) {
+    if (idle != 0 && st.cursor < st.len) {
       const uint32_t rank = __popc(idle & lt_mask);
       const uint32_t fresh = __shfl_sync(kFullMask, ahead, rank);
-      if (!have && sl.cursor + rank < sl.len) {
+      if (!have && st.cursor + rank < st.len) {
         key = fresh;
-        idx = sl.cursor + rank;
+        idx = st.at(st.cursor + rank);
         round = 0;
         have = true;
       }
-      sl.cursor = min(sl.cursor + __popc(idle), sl.len);
-      ahead = sl.cursor + lane < sl.len ? __ldg(keys + sl.cursor + lane) : 0u;
+      st.cursor = min(st.cursor + __popc(idle), st.len);
+      ahead = st.cursor + lane < st.len ? __ldg(keys + st.at(st.cursor + lane)) : 0u;
     }
     if (!__any_sync(kFullMask, have)) break;
 

@@ -28,35 +28,37 @@ __device__ __forceinline__ void flush_insert_counters(DevCounters* ctr, int lane
 // The (key, value) stream of one warp: the next 32 pairs of the warp's slice are prefetched one
 // round ahead; idle lanes take them in order.
 struct PairFeed {
-  Slice sl;
-  const uint32_t* keys;    // slice-relative
+  Stream st;
+  const uint32_t* keys;
   const uint32_t* values;
   uint32_t ahead_k, ahead_v;
 
   __device__ __forceinline__ void init(const uint32_t* __restrict__ k, const uint32_t* __restrict__ v, uint64_t n, int lane) {
-    sl = warp_slice(n);
-    keys = k + sl.start;
-    values = v + sl.start;
+    st = warp_stream(n);
+    keys = k;
+    values = v;
     prefetch(lane);
   }
   __device__ __forceinline__ void prefetch(int lane) {
-    const bool in = sl.cursor + lane < sl.len;
-    ahead_k = in ? __ldg(keys + sl.cursor + lane) : 0u;
-    ahead_v = in ? __ldg(values + sl.cursor + lane) : 0u;
+    const uint32_t p = st.cursor + lane;
+    const bool in = p < st.len;
+    const uint64_t g = st.at(p);
+    ahead_k = in ? __ldg(keys + g) : 0u;
+    ahead_v = in ? __ldg(values + g) : 0u;
   }
   // Returns true for lanes that received a fresh pair.
   __device__ __forceinline__ bool refill(bool have, int lane, uint32_t& key, uint32_t& val) {
     const uint32_t idle = __ballot_sync(kFullMask, !have);
-    if (idle == 0 || sl.cursor >= sl.len) return false;
+    if (idle == 0 || st.cursor >= st.len) return false;
     const uint32_t rank = __popc(idle & ((1u << lane) - 1u));
     const uint32_t fk = __shfl_sync(kFullMask, ahead_k, rank);
     const uint32_t fv = __shfl_sync(kFullMask, ahead_v, rank);
-    const bool got = !have && sl.cursor + rank < sl.len;
+    const bool got = !have && st.cursor + rank < st.len;
     if (got) {
       key = fk;
       val = fv;
     }
-    sl.cursor = min(sl.cursor + __popc(idle), sl.len);
+    st.cursor = min(st.cursor + __popc(idle), st.len);
     prefetch(lane);
     return got;
   }

@@ -121,6 +121,38 @@ __device__ __forceinline__ void fetch_wait() {
   __syncwarp();
 }
 
+// ---- load of a staged bucket (insert side) ------------------------------------------------------
+// Slots are only ever claimed at index = load (table.cpp:85) and full buckets never drain, so the
+// occupied slots of a bucket are a prefix and compute_load's popcount (bucket.hpp:26-31) equals the
+// index of the first empty slot.  That index is found with a 4-ary search: 4 independent 4-byte
+// reads per level instead of B reads in total (b = 16: 4 + 3 reads, two dependent levels).
+__device__ __forceinline__ uint32_t staged_key(uint32_t base, uint32_t slot) {
+  return lds_u32((base ^ ((slot >> 1) << 4)) + ((slot & 1u) << 3));
+}
+// occupied slots among [lo, lo + L - 1), given that slot lo + L - 1 is empty
+template <int L>
+__device__ __forceinline__ uint32_t prefix_below(uint32_t base, uint32_t lo) {
+  if constexpr (L == 1) {
+    return 0;
+  } else if constexpr (L == 2) {
+    return staged_key(base, lo) != kEmptyKey;
+  } else {
+    constexpr int Q = L / 4;
+    const uint32_t a = staged_key(base, lo + Q - 1), b = staged_key(base, lo + 2 * Q - 1), c = staged_key(base, lo + 3 * Q - 1);
+    const uint32_t q = (a != kEmptyKey) + (b != kEmptyKey) + (c != kEmptyKey);
+    return q * Q + prefix_below<Q>(base, lo + q * Q);
+  }
+}
+template <int B>
+__device__ __forceinline__ uint32_t staged_prefix_load(uint32_t base) {
+  constexpr int S = B / 4;
+  const uint32_t a = staged_key(base, S - 1), b = staged_key(base, 2 * S - 1), c = staged_key(base, 3 * S - 1),
+                 d = staged_key(base, 4 * S - 1);
+  const uint32_t q = (a != kEmptyKey) + (b != kEmptyKey) + (c != kEmptyKey) + (d != kEmptyKey);
+  if (q == 4) return B;
+  return q * S + prefix_below<S>(base, q * S);
+}
+
 // ---- scan -------------------------------------------------------------------------------------
 // The lane's own bucket: staged sizes read row `lane` of `stage`; b <= 2 loads straight from
 // global memory through L2.  WANT_KEY = false skips the key match (insert needs the load only).
@@ -166,18 +198,7 @@ __device__ __forceinline__ Scan scan_bucket(uint32_t stage, const uint64_t* __re
       r.found = value != kEmptyKey;
       r.load = top == kEmptyKey ? 0u : static_cast<uint32_t>(B);  // only full / not full is reported
     } else {
-      // insert: the load is the index of the first empty slot.  Slots are only ever claimed at index
-      // = load (table.cpp:85) and full buckets never drain, so the occupied slots of a bucket are a
-      // prefix and compute_load's popcount (bucket.hpp:26-31) equals this binary search: log2(B)+1
-      // 4-byte reads instead of B.
-      auto key_at = [&](uint32_t i) { return lds_u32((base ^ ((i >> 1) << 4)) + ((i & 1u) << 3)); };
-      uint32_t pos = 0;
-#pragma unroll
-      for (int step = B / 2; step >= 1; step >>= 1) {
-        if (key_at(pos + step - 1) != kEmptyKey) pos += step;
-      }
-      if (key_at(pos) != kEmptyKey) pos += 1;
-      r.load = pos;
+      r.load = staged_prefix_load<B>(base);
     }
   }
   return r;
@@ -238,23 +259,35 @@ __device__ __forceinline__ uint64_t pack_pair(uint32_t key, uint32_t value) {
 }
 
 // ---- work distribution ------------------------------------------------------------------------
-// Every warp owns one contiguous slice of the input and streams through it as a lane-level state
-// machine: a lane that has finished its key takes the next unread key of the slice, so every probe
-// round is dense (32 probes per warp) no matter how many rounds individual keys need.  The next 32
-// keys of the slice are prefetched one round ahead and handed out with a shuffle.
-struct Slice {
-  uint64_t start;        // first element of the warp's slice
-  uint32_t len, cursor;  // slice length and next unread element, relative to start
+// The input is cut into chunks of kChunk elements that are dealt round-robin to the warps of the
+// grid, so at any moment the keys in flight form one narrow window that slides over the input (input
+// that is grouped by table region therefore probes one L2-sized region at a time).  Every warp streams
+// through its chunks as a lane-level state machine: a lane that has finished its key takes the next
+// unread key of the warp's stream, so every probe round is dense (32 probes per warp) no matter how
+// many rounds individual keys need.  The next 32 keys of the stream are prefetched one round ahead and
+// handed out with a shuffle.
+constexpr uint32_t kChunk = 256;
+
+struct Stream {
+  uint32_t warp, n_warps;
+  uint32_t len, cursor;  // stream length and next unread position, in stream coordinates
+
+  // position in the warp's stream -> index into the caller's arrays
+  __device__ __forceinline__ uint64_t at(uint32_t p) const {
+    return (static_cast<uint64_t>(p / kChunk) * n_warps + warp) * kChunk + (p % kChunk);
+  }
 };
 
-__device__ __forceinline__ Slice warp_slice(uint64_t n) {
-  const uint64_t warp = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const uint64_t n_warps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
-  uint64_t len = (n + n_warps - 1) / n_warps;
-  len = (len + 31) & ~31ull;  // whole 128-byte lines of keys per warp
-  Slice s;
-  s.start = warp * len < n ? warp * len : n;
-  s.len = static_cast<uint32_t>(s.start + len < n ? len : n - s.start);
+__device__ __forceinline__ Stream warp_stream(uint64_t n) {
+  Stream s;
+  s.warp = static_cast<uint32_t>((static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5);
+  s.n_warps = static_cast<uint32_t>((static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5);
+  const uint64_t chunks = (n + kChunk - 1) / kChunk;
+  const uint64_t mine = s.warp < chunks ? (chunks - s.warp + s.n_warps - 1) / s.n_warps : 0;
+  uint64_t len = mine * kChunk;
+  // the globally last chunk may be partial; it is the last chunk of whichever warp owns it
+  if (mine != 0 && ((mine - 1) * s.n_warps + s.warp) == chunks - 1) len -= chunks * kChunk - n;
+  s.len = static_cast<uint32_t>(len);
   s.cursor = 0;
   return s;
 }

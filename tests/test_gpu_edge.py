@@ -1,0 +1,237 @@
+"""Edge cases of the CUDA path that the reference tests cover: empty and ragged inputs, the sentinel, error
+behaviour, builds that fail, stability, single-bucket contention, store interchange, multi-call builds."""
+import os
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, random_values, to_oracle_cfg, unique_keys
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+EMPTY = 0xFFFFFFFF
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a).view(np.int32)).cuda()
+
+
+def host(t):
+    return t.cpu().numpy().view(np.uint32)
+
+
+def packed(keys, values):
+    return np.sort((values.astype(np.uint64) << np.uint64(32)) | keys.astype(np.uint64))
+
+
+def stored(table):
+    s = table.download_store()
+    return np.sort(s[s != np.uint64(0xFFFFFFFFFFFFFFFF)])
+
+
+def test_empty_and_ragged_sizes(bht):
+    # test_table.cpp:208-216 (empty key set) and ragged tails around the warp / chunk sizes
+    cfg = bht.make_config("bcht", 300_000, 0.8, 16, seed=2)
+    table = bht.HashTable(cfg, 0)
+    o = table.insert(np.empty(0, dtype=np.uint32), np.empty(0, dtype=np.uint32))
+    assert o.success and o.inserted == 0 and o.probes == 0
+    assert table.find(np.empty(0, dtype=np.uint32)).size == 0
+    keys = unique_keys(250_000, 9)
+    vals = random_values(250_000, 9)
+    lo = 0
+    for n in [1, 31, 32, 33, 255, 256, 257, 1023, 8191, 8193, 100_003]:
+        o = table.insert(dev(keys[lo:lo + n]), dev(vals[lo:lo + n]))
+        assert o.success and o.inserted == n and o.attempted == n
+        lo += n
+    assert table.inserted() == lo == table.occupied_slots()
+    for n in [1, 31, 33, 257, 100_003, lo]:
+        assert np.array_equal(host(table.find(dev(keys[:n]))), vals[:n])
+        assert np.array_equal(table.find(keys[lo - n:lo]), vals[lo - n:lo])  # host path
+    assert np.all(host(table.find(dev(keys[lo:lo + 5000]))) == EMPTY)
+    table.clear()
+    assert table.inserted() == 0 and table.occupied_slots() == 0
+    assert np.all(host(table.find(dev(keys[:1000]))) == EMPTY)
+
+
+def test_sentinel_query_and_duplicates_in_query(bht):
+    cfg = bht.make_config("bcht", 1000, 0.5, 16, seed=3)
+    table, o = bht.build(np.arange(1000, dtype=np.uint32), cfg, np.arange(1000, dtype=np.uint32) + 5, device=0)
+    assert o.success
+    q = np.array([EMPTY, 7, 7, 7, EMPTY, 999, 1000, 0], dtype=np.uint32)
+    assert list(table.find(q)) == [EMPTY, 12, 12, 12, EMPTY, 1004, EMPTY, 5]
+
+
+def test_error_behaviour(bht):
+    cfg = bht.make_config("bcht", 16, 1.0, 16, seed=1)
+    with pytest.raises(bht.CapacityError):  # table.cpp:225
+        bht.build(np.arange(17, dtype=np.uint32), cfg, device=0)
+    table = bht.HashTable(cfg, 0)
+    with pytest.raises(bht.CapacityError):
+        table.insert(np.arange(17, dtype=np.uint32), np.arange(17, dtype=np.uint32))
+    bad = cfg.copy()
+    bad.n_hashes = 2
+    with pytest.raises(ValueError):  # table.cpp:22-23
+        bht.HashTable(bad, 0)
+    with pytest.raises(bht.KindMismatchError):  # require_kind, table.cpp:15-17
+        table.insert(np.arange(4, dtype=np.uint32), np.arange(4, dtype=np.uint32), as_kind="bp2ht")
+    with pytest.raises(bht.KindMismatchError):
+        table.find(np.arange(4, dtype=np.uint32), as_kind="iht")
+    with pytest.raises(bht.KindMismatchError):
+        table.set_iht_prose_fallback(True)
+    assert table.insert(np.arange(4, dtype=np.uint32), np.arange(4, dtype=np.uint32), as_kind="bcht").success
+    one = bht.HashTable(bht.make_config("1cht", 100, 0.5, 1, seed=1), 0)
+    assert one.insert(np.arange(4, dtype=np.uint32), np.arange(4, dtype=np.uint32), as_kind="bcht").success  # table.cpp:55
+    with pytest.raises(ValueError):
+        table.insert(dev(np.arange(4, dtype=np.uint32)), np.arange(4, dtype=np.uint32))  # mixed memory spaces
+    with pytest.raises(ValueError):
+        table.find(np.arange(4, dtype=np.float32))
+    # a full table: further inserts fail like insert_pair does, they are not an error
+    o = table.insert(np.arange(100, 120, dtype=np.uint32), np.arange(20, dtype=np.uint32))
+    assert not o.success and o.failed >= 8 and o.inserted <= 12
+
+
+@pytest.mark.parametrize("kind,b,lf,t,max_chain", [("bp2ht", 8, 1.0, None, None), ("bp2ht", 16, 0.95, None, None),
+                                                   ("iht", 16, 0.99, None, None), ("iht", 16, 0.9, 3, None),
+                                                   ("bcht", 16, 0.999, None, 2), ("1cht", 1, 0.97, None, 6),
+                                                   ("bcht", 4, 0.98, None, 1)])
+def test_failed_builds_are_reported_consistently(bht, ora, kind, b, lf, t, max_chain):
+    """Cells that do not build (SURVEY 'infeasible cells'): success=false, every dropped key is absent, every other key
+    is found with its value, stored multiset == input minus dropped."""
+    n = 80_000
+    keys = unique_keys(n, 31 + b)
+    vals = random_values(n, b)
+    cfg = bht.make_config(kind, n, lf, b, threshold=t, seed=17, max_chain=max_chain)
+    table, o = bht.build(dev(keys), cfg, dev(vals), device=0)
+    assert not o.success and o.failed > 0 and o.inserted + o.failed == n and o.attempted == n
+    dropped = table.failed_keys()
+    assert dropped.size == o.failed and np.unique(dropped).size == dropped.size
+    assert o.failed_key in set(dropped.tolist())
+    assert np.isin(dropped, keys).all()
+    got = host(table.find(dev(keys)))
+    is_dropped = np.isin(keys, dropped)
+    assert np.all(got[is_dropped] == EMPTY)
+    assert np.array_equal(got[~is_dropped], vals[~is_dropped])
+    assert np.array_equal(stored(table), packed(keys[~is_dropped], vals[~is_dropped]))
+    assert table.inserted() == o.inserted == table.occupied_slots()
+    assert table.count_inadmissible() == 0
+    # the reference fails on the same cell (not necessarily on the same keys)
+    ot = ora.table(to_oracle_cfg(cfg))
+    assert not ot.build(keys, vals)["success"]
+    # and agrees with the GPU about every query on the GPU-built layout
+    ot.upload_store(table.download_store())
+    want, _, _ = ot.find_bulk(keys)
+    assert np.array_equal(got, want)
+
+
+def test_single_bucket_contention_claims_exactly_b(bht):
+    # acceptance.cpp:425-457 / test_bucket.cpp:79-95: many concurrent claimants, one bucket -> exactly b winners
+    for kind, hashes in [("bp2ht", [(1, 0, 1), (1, 0, 1)]), ("iht", [(1, 0, 1)] * 3), ("bcht", [(1, 0, 1)] * 3)]:
+        for b in [1, 2, 16, 64] if kind != "iht" else [2, 16, 64]:
+            cfg = bht.craft_config(kind, 1, b, hashes, threshold=max(1, b // 2), max_chain=3)
+            table = bht.HashTable(cfg, 0)
+            n = 20_000
+            keys = np.arange(1, n + 1, dtype=np.uint32)
+            o = table.insert(dev(keys), dev(keys ^ np.uint32(0xABCD)))
+            assert o.inserted == b and o.failed == n - b, (kind, b, o)
+            s = table.download_store()
+            k = (s & np.uint64(0xFFFFFFFF)).astype(np.uint32)
+            v = (s >> np.uint64(32)).astype(np.uint32)
+            assert np.unique(k).size == b and np.all(k != EMPTY)
+            assert np.array_equal(v, k ^ np.uint32(0xABCD))  # no torn pairs (test_bucket.cpp:97-124)
+
+
+@pytest.mark.parametrize("kind,b,lf", [("bp2ht", 16, 0.8), ("iht", 16, 0.8), ("bp2ht", 32, 0.85)])
+def test_stability_placed_pairs_never_move(bht, kind, b, lf):
+    # test_table.cpp:262-284, acceptance.cpp:392-422
+    n = 100_000
+    keys = unique_keys(n, 55)
+    vals = random_values(n, 55)
+    table = bht.HashTable(bht.make_config(kind, n, lf, b, seed=8), 0)
+    assert table.insert(dev(keys[:n // 2]), dev(vals[:n // 2])).success
+    before = table.download_store()
+    assert table.insert(dev(keys[n // 2:]), dev(vals[n // 2:])).success
+    after = table.download_store()
+    occupied = before != np.uint64(0xFFFFFFFFFFFFFFFF)
+    assert np.array_equal(after[occupied], before[occupied])
+
+
+def test_store_interchange_and_dump(bht, ora, tmp_path):
+    n = 30_000
+    keys = unique_keys(n, 66)
+    cfg = bht.make_config("iht", n, 0.8, 16, seed=4)
+    table, o = bht.build(dev(keys), cfg, device=0)
+    assert o.success
+    path = tmp_path / "store.bin"
+    table.dump_store(str(path))  # table.cpp:41-51: LE u64 per slot, bucket order
+    raw = np.fromfile(path, dtype="<u8")
+    assert np.array_equal(raw, table.download_store())
+    with pytest.raises(OSError):
+        table.dump_store(str(tmp_path / "no_such_dir" / "x.bin"))
+    # slot_at / poke_slot (table.hpp:53-56): corrupt one value, the oracle's checker sees exactly one wrong value
+    ot = ora.table(to_oracle_cfg(cfg))
+    idx = int(np.nonzero(raw != np.uint64(0xFFFFFFFFFFFFFFFF))[0][5])
+    slot = table.slot_at(idx)
+    assert slot == int(raw[idx])
+    k = slot & 0xFFFFFFFF
+    table.poke_slot(idx, bht.pack_pair(k, 12345))
+    assert host(table.find(dev(np.array([k], dtype=np.uint32))))[0] == 12345
+    ot.upload_store(table.download_store())
+    want, _, _ = ot.find_bulk(keys)
+    assert int((want != ora.values_for_keys(keys)).sum()) == 1  # test_oracle.cpp:29-46 shape
+    # a foreign key poked into a bucket it does not hash to is an admissibility violation (test_oracle.cpp:48-64)
+    empty_idx = int(np.nonzero(raw == np.uint64(0xFFFFFFFFFFFFFFFF))[0][0])
+    foreign = next(x for x in range(1, 1000) if all(table.bucket_of(i, x) != empty_idx // 16 for i in range(3)))
+    table.poke_slot(empty_idx, bht.pack_pair(foreign, 1))
+    assert table.count_inadmissible() == 1
+
+
+def test_multi_stream_concurrent_finds(bht):
+    n = 400_000
+    keys = unique_keys(n, 88)
+    vals = random_values(n, 88)
+    table, o = bht.build(dev(keys), bht.make_config("bcht", n, 0.9, 16, seed=6), dev(vals), device=0)
+    assert o.success
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream() for _ in range(4)]
+    outs = []
+    dk = dev(keys)
+    for i, s in enumerate(streams):
+        with torch.cuda.stream(s):
+            outs.append(table.find(dk[i::4].contiguous(), stream=s))
+    torch.cuda.synchronize()
+    for i, o_ in enumerate(outs):
+        assert np.array_equal(host(o_), vals[i::4])
+
+
+def test_device_key_generator_and_shard_routing(bht):
+    from paper_2108_07232_b200 import _lib
+    lib = _lib.load()
+    seed = 0x1234ABCD5678
+    k, v = bht.generate_unique_keys(seed, 1000, 1 << 20, device=0)
+    k, v = host(k), host(v)
+    assert np.unique(k).size == k.size and not np.any(k == EMPTY) and not np.any(v == EMPTY)
+    assert [int(x) for x in k[:50]] == [lib.bht_unique_key_host(seed, 1000 + i) for i in range(50)]
+    assert [int(x) for x in v[:50]] == [lib.bht_synthetic_value_host(seed, int(x)) for x in k[:50]]
+    with pytest.raises(ValueError):
+        bht.generate_unique_keys(seed, 0xFFFFFFF0, 100, device=0)
+    # K8 partition + K9 un-permute against numpy
+    a, b = bht.shard_constants(5)
+    ops = bht.CudaShardOps(bht.make_config("bcht", 1000, 0.5, 16, seed=1), 0)
+    for n_shards in [1, 2, 8, 7]:
+        dk, dv = dev(k), dev(v)
+        pk, pv, idx, counts = ops.partition(a, b, n_shards, dk, dv, True)
+        owner = np.array([lib.bht_shard_of_host(a, b, n_shards, int(x)) for x in k[:2000]])
+        pk, pv, idx = host(pk), host(pv), host(idx).astype(np.int64)
+        assert sum(counts) == k.size
+        assert np.array_equal(k[idx], pk) and np.array_equal(v[idx], pv)  # routed element i came from position idx[i]
+        assert np.unique(idx).size == k.size
+        bounds = np.cumsum([0] + counts)
+        full_owner = ((((a * k.astype(object) + b) % 4294967291) * n_shards) >> 32).astype(np.int64) if k.size <= 4096 else None
+        for s in range(n_shards):
+            seg = pk[bounds[s]:bounds[s + 1]]
+            sample = seg[:: max(1, seg.size // 200)]
+            assert all(lib.bht_shard_of_host(a, b, n_shards, int(x)) == s for x in sample)
+        assert np.array_equal(np.bincount(owner, minlength=n_shards)[:n_shards] > 0, np.array(counts) > 0) or n_shards > 2
+        out = torch.empty(k.size, dtype=torch.int32, device="cuda")
+        ops.unpermute(dev(pv), dev(idx.astype(np.uint32)), out)
+        assert np.array_equal(host(out), v)
