@@ -142,7 +142,7 @@ int32_t bht_device_of(const bht_table* table);
 /* Bulk insert: replaces build()'s insertion loop (table.cpp:224-271) and insert_pair
  * (table.cpp:203-212) with explicit values.  Precondition as in the reference: keys unique,
  * != sentinel, not yet present.  Unlike the reference's build, which stops at the first failed
- * key, every pair is attempted.  BHT_CAPACITY_EXCEEDED when n > capacity (build's check, table.cpp:225).
+ * key, every pair is attempted; pairs that do not fit are reported in `result`, not as an error.
  * `result` may be NULL (no synchronisation; fetch it later with bht_last_insert_result). */
 bht_status bht_insert(bht_table* table, const uint32_t* keys, const uint32_t* values, uint64_t n,
                       int32_t mem_space, bht_insert_result* result, void* stream);
@@ -152,6 +152,13 @@ bht_status bht_insert(bht_table* table, const uint32_t* keys, const uint32_t* va
  * out_values[i] = value, or BHT_EMPTY_VALUE when the key is absent. */
 bht_status bht_find(const bht_table* table, const uint32_t* keys, uint32_t* out_values, uint64_t n,
                     int32_t mem_space, bht_find_result* result, void* stream);
+
+/* build(keys, cfg, opts) (table.hpp:125-127, table.cpp:224-276) in one call: BHT_CAPACITY_EXCEEDED when
+ * n > cfg->capacity ("build: key set exceeds table capacity", table.cpp:225, checked before anything is
+ * allocated), else bht_create + bht_insert of all n pairs.  *out receives the new table. */
+bht_status bht_build(const bht_config* cfg, int32_t device, const uint32_t* keys, const uint32_t* values,
+                     uint64_t n, int32_t mem_space, int32_t iht_prose_fallback, bht_table** out,
+                     bht_insert_result* result, void* stream);
 
 /* The reference's per-variant entry points bcht_insert / bp2ht_insert / iht_insert and bcht_find /
  * bp2ht_find / iht_find (table.hpp:84-101): as bht_insert / bht_find, but BHT_KIND_MISMATCH when the

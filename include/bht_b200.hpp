@@ -99,6 +99,7 @@ struct build_options {
 class hash_table {
  public:
   explicit hash_table(const table_config& cfg, int device = 0) : cfg_(cfg) { check(bht_create(&cfg_, device, &h_)); }
+  hash_table(bht_table* adopted, const table_config& cfg) : cfg_(cfg), h_(adopted) {}  // takes ownership (bht_build)
   ~hash_table() { bht_destroy(h_); }
   hash_table(const hash_table&) = delete;
   hash_table& operator=(const hash_table&) = delete;
@@ -215,7 +216,6 @@ class hash_table {
 
   bht_table* handle() const { return h_; }
 
- private:
   static build_outcome outcome_of(const bht_insert_result& r) {
     build_outcome o;
     o.success = r.success != 0;
@@ -226,6 +226,8 @@ class hash_table {
     if (r.first_failed_key != BHT_EMPTY_KEY) o.failed_key = r.first_failed_key;
     return o;
   }
+
+ private:
   table_config cfg_;
   bht_table* h_ = nullptr;
 };
@@ -234,13 +236,23 @@ class hash_table {
 inline std::pair<hash_table, build_outcome> build(const key_type* keys, std::uint64_t n, const table_config& cfg,
                                                   build_options opts = {}) {
   if (n > cfg.capacity) throw std::invalid_argument("build: key set exceeds table capacity");
-  if (opts.space != mem_space::host) throw std::invalid_argument("build: derives values on the host; pass host keys or use insert()");
-  hash_table table(cfg, opts.device);
-  if (opts.iht_prose_fallback) table.set_iht_prose_fallback(true);
+  if (opts.space != mem_space::host) throw std::invalid_argument("build: derives values on the host; pass host keys or use build_pairs()");
   std::vector<value_type> values(n);
   for (std::uint64_t i = 0; i < n; ++i) values[i] = value_for_key(keys[i]);
-  build_outcome o = table.insert(keys, values.data(), n, mem_space::host, opts.stream);
-  return {std::move(table), o};
+  bht_table* h = nullptr;
+  bht_insert_result r{};
+  check(bht_build(&cfg, opts.device, keys, values.data(), n, BHT_MEM_HOST, opts.iht_prose_fallback ? 1 : 0, &h, &r, opts.stream));
+  return {hash_table(h, cfg), hash_table::outcome_of(r)};
+}
+
+// build with explicit values, in either memory space
+inline std::pair<hash_table, build_outcome> build_pairs(const key_type* keys, const value_type* values, std::uint64_t n,
+                                                        const table_config& cfg, build_options opts = {}) {
+  bht_table* h = nullptr;
+  bht_insert_result r{};
+  check(bht_build(&cfg, opts.device, keys, values, n, static_cast<std::int32_t>(opts.space), opts.iht_prose_fallback ? 1 : 0, &h, &r,
+                  opts.stream));
+  return {hash_table(h, cfg), hash_table::outcome_of(r)};
 }
 
 }  // namespace gpu

@@ -96,6 +96,8 @@ SIGNATURES = {
     "bht_get_config": (C.c_int, [_vp, C.POINTER(Config)]),
     "bht_device_of": (C.c_int32, [_vp]),
     "bht_insert": (C.c_int, [_vp, _vp, _vp, C.c_uint64, C.c_int32, C.POINTER(InsertResult), _vp]),
+    "bht_build": (C.c_int, [C.POINTER(Config), C.c_int32, _vp, _vp, C.c_uint64, C.c_int32, C.c_int32, C.POINTER(_vp),
+                            C.POINTER(InsertResult), _vp]),
     "bht_insert_as": (C.c_int, [_vp, C.c_int32, _vp, _vp, C.c_uint64, C.c_int32, C.POINTER(InsertResult), _vp]),
     "bht_find": (C.c_int, [_vp, _vp, _vp, C.c_uint64, C.c_int32, C.POINTER(FindResult), _vp]),
     "bht_find_as": (C.c_int, [_vp, C.c_int32, _vp, _vp, C.c_uint64, C.c_int32, C.POINTER(FindResult), _vp]),

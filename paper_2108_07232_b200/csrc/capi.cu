@@ -203,10 +203,6 @@ bht_status do_insert(bht_table* t, const uint32_t* keys, const uint32_t* values,
   std::lock_guard<std::mutex> lock(t->mu);
   cudaStream_t stream = as_stream(stream_v);
 
-  // build(): "key set exceeds table capacity" (table.cpp:225).  Like insert_pair, a call that merely
-  // overfills an already loaded table is attempted and reports its failures in the result.
-  if (n > t->cfg.capacity) return fail(BHT_CAPACITY_EXCEEDED, "build: key set exceeds table capacity");
-
   BHT_CUDA(cudaMemsetAsync(t->ctr, 0, kPerCallCounterBytes, stream));
   if (mem_space == BHT_MEM_DEVICE) {
     BHT_CUDA(launch_insert_kind(t, keys, values, n, stream));
@@ -474,6 +470,25 @@ int32_t bht_device_of(const bht_table* t) { return t ? t->device : -1; }
 bht_status bht_insert(bht_table* t, const uint32_t* keys, const uint32_t* values, uint64_t n, int32_t mem_space,
                       bht_insert_result* result, void* stream) {
   return do_insert(t, keys, values, n, mem_space, result, stream);
+}
+
+bht_status bht_build(const bht_config* cfg, int32_t device, const uint32_t* keys, const uint32_t* values, uint64_t n,
+                     int32_t mem_space, int32_t iht_prose_fallback, bht_table** out, bht_insert_result* result, void* stream) {
+  if (cfg == nullptr || out == nullptr) return fail(BHT_INVALID_ARGUMENT, "bht_build: null argument");
+  *out = nullptr;
+  // build(): the capacity check comes before the table exists (table.cpp:225)
+  if (n > cfg->capacity) return fail(BHT_CAPACITY_EXCEEDED, "build: key set exceeds table capacity");
+  bht_table* t = nullptr;
+  bht_status s = bht_create(cfg, device, &t);
+  if (s != BHT_OK) return s;
+  if (iht_prose_fallback && cfg->kind == BHT_IHT) t->view.prose = 1u;
+  s = do_insert(t, keys, values, n, mem_space, result, stream);
+  if (s != BHT_OK) {
+    bht_destroy(t);
+    return s;
+  }
+  *out = t;
+  return BHT_OK;
 }
 
 bht_status bht_insert_as(bht_table* t, int32_t kind, const uint32_t* keys, const uint32_t* values, uint64_t n,

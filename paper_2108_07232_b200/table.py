@@ -221,6 +221,16 @@ class HashTable:
         self._cfg = cfg.copy()
         _check(self._lib.bht_create(C.byref(self._cfg), self.device, C.byref(self._h)))
 
+    @classmethod
+    def _adopt(cls, handle, cfg: Config, device: int) -> "HashTable":
+        """Wraps a table created by the library (bht_build)."""
+        self = cls.__new__(cls)
+        self._lib = _lib.load()
+        self._h = handle
+        self.device = device
+        self._cfg = cfg.copy()
+        return self
+
     # -- lifetime
     def close(self) -> None:
         if getattr(self, "_h", None) is not None and self._h:
@@ -407,13 +417,22 @@ def build(keys, cfg: Config, values=None, device: Optional[int] = None, iht_pros
     Unlike the reference, which stops at the first failed key, every key is attempted; ``success`` still means
     inserted == len(keys).  Raises CapacityError when len(keys) > capacity, before touching the device store.
     """
-    n = keys.numel() if isinstance(keys, torch.Tensor) else len(keys)
-    if n > cfg.capacity:
-        raise CapacityError("build: key set exceeds table capacity")
-    table = HashTable(cfg, device)
-    if iht_prose_fallback:
-        table.set_iht_prose_fallback(True)
-    outcome = table.insert(keys, values, stream=stream)
+    if values is None:
+        values = values_for_keys(keys)
+    kp, kn, kspace, _k = _as_u32(keys, "keys")
+    vp, vn, vspace, _v = _as_u32(values, "values")
+    if kspace != vspace or kn != vn:
+        raise ValueError("build: keys and values must have the same length and memory space")
+    if device is None:
+        device = keys.device.index if isinstance(keys, torch.Tensor) and keys.is_cuda else (
+            torch.cuda.current_device() if torch.cuda.is_available() else 0)
+    handle = C.c_void_p()
+    res = InsertResult()
+    _check(_lib.load().bht_build(C.byref(cfg), int(device), kp, vp, kn, kspace, int(bool(iht_prose_fallback)),
+                                 C.byref(handle), C.byref(res), _stream_ptr(stream, int(device))))
+    table = HashTable._adopt(handle, cfg, int(device))
+    outcome = BuildOutcome(bool(res.success), res.inserted, res.failed, res.attempted, res.probes,
+                           None if res.first_failed_key == EMPTY_KEY else res.first_failed_key)
     return table, outcome
 
 

@@ -66,8 +66,6 @@ def test_error_behaviour(bht):
     with pytest.raises(bht.CapacityError):  # table.cpp:225
         bht.build(np.arange(17, dtype=np.uint32), cfg, device=0)
     table = bht.HashTable(cfg, 0)
-    with pytest.raises(bht.CapacityError):
-        table.insert(np.arange(17, dtype=np.uint32), np.arange(17, dtype=np.uint32))
     bad = cfg.copy()
     bad.n_hashes = 2
     with pytest.raises(ValueError):  # table.cpp:22-23
@@ -86,12 +84,12 @@ def test_error_behaviour(bht):
     with pytest.raises(ValueError):
         table.find(np.arange(4, dtype=np.float32))
     # a full table: further inserts fail like insert_pair does, they are not an error
-    o = table.insert(np.arange(100, 120, dtype=np.uint32), np.arange(20, dtype=np.uint32))
-    assert not o.success and o.failed >= 8 and o.inserted <= 12
+    o = table.insert(np.arange(100, 116, dtype=np.uint32), np.arange(16, dtype=np.uint32))
+    assert not o.success and o.failed >= 4 and o.inserted <= 12 and o.inserted + o.failed == 16
 
 
 @pytest.mark.parametrize("kind,b,lf,t,max_chain", [("bp2ht", 8, 1.0, None, None), ("bp2ht", 16, 0.95, None, None),
-                                                   ("iht", 16, 0.99, None, None), ("iht", 16, 0.9, 3, None),
+                                                   ("iht", 16, 0.99, None, None), ("iht", 16, 0.97, 3, None),
                                                    ("bcht", 16, 0.999, None, 2), ("1cht", 1, 0.97, None, 6),
                                                    ("bcht", 4, 0.98, None, 1)])
 def test_failed_builds_are_reported_consistently(bht, ora, kind, b, lf, t, max_chain):

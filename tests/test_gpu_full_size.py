@@ -50,13 +50,13 @@ def test_full_size_properties(bht, workload, kind, b, lf, t, ref_probes):
     assert torch.equal(out, values)
     _, st0 = table.find(absent, out, want_stats=True)
     assert st0.hits == 0 and bool((out == -1).all())
-    half = torch.cat([present[: N // 2], absent[: N // 2]])
+    half = torch.cat([present[::2], absent[::2]]).contiguous()  # a uniform sample: early-inserted keys were evicted more
     _, st50 = table.find(half, out, want_stats=True)
     assert st50.hits == N // 2
     # hardware-independent probe means (concurrent insertion re-probes after lost races, so insert may sit a little
     # above the sequential reference; finds are deterministic given the layout statistics)
     ins, f100, f0 = ref_probes
-    assert ins - 0.01 <= o.mean_probes <= ins + 0.05, (o.mean_probes, ins)
+    assert 0.985 * ins <= o.mean_probes <= 1.03 * ins + 0.03, (o.mean_probes, ins)
     assert abs(st.mean_probes - f100) < 0.02, (st.mean_probes, f100)
     assert abs(st0.mean_probes - f0) < 0.03, (st0.mean_probes, f0)
     assert abs(st50.mean_probes - (f100 + f0) / 2) < 0.03
