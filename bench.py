@@ -148,7 +148,7 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32/u64 integer",
         "data": "synthetic: unique uniform u32 keys, MT19937",
-        "config": workload_config(n, args.gpus),
+        "config": workload_config(n, args.gpus, ocfg.capacity * 8 / 1e6),
         "cpu_baseline": {"value": value, "unit": "MKeys/s", "cores": threads, "kind": "reference", "sample": sample,
                          "insert_mkeys": n_sample * args.steps / sum(tbs) / 1e6,
                          "find_mkeys": n_sample * args.steps / sum(tfs) / 1e6},
@@ -165,10 +165,10 @@ def make_ref_config(ref, n):
     return cfg
 
 
-def workload_config(n, gpus):
+def workload_config(n, gpus, table_mb=None):
     return {"workload": f"{KIND} b={B}, {n} unique u32 keys/values per GPU, load factor {LF}: bulk build then "
                         f"{n} positive bulk finds", "kind": KIND, "bucket_size": B, "load_factor": LF,
-            "keys_per_gpu": n, "table_mb": None, "l2": "table and inputs each exceed the 126 MB L2; no flush needed",
+            "keys_per_gpu": n, "table_mb": table_mb, "l2": "table and inputs each exceed the 126 MB L2; no flush needed",
             "parallelism": "single table" if gpus == 1 else f"key-range sharded x{gpus}, NCCL all-to-all"}
 
 
@@ -211,10 +211,18 @@ def run_cuda(args):
     sampler = ClockSampler(local)
 
     if world == 1:
-        present, absent, values = make_workload(n, SEED)
-        d_keys = torch.from_numpy(present.view(np.int32)).to(device)
-        d_vals = torch.from_numpy(values.view(np.int32)).to(device)
-        d_abs = torch.from_numpy(absent.view(np.int32)).to(device)
+        if args.device_keys:
+            # sizes where the MT19937 host generator is impractical (the 5*10^8-key shard of the 4-billion-key
+            # configuration): keys / values from the device bijection, negatives = the next n counters
+            dk, dv = bht.generate_unique_keys(SEED, 0, n, device=local)
+            da = bht.generate_unique_keys(SEED, n, n, device=local, with_values=False)
+            d_keys, d_vals, d_abs = dk.view(torch.int32), dv.view(torch.int32), da.view(torch.int32)
+            present, values, absent = None, None, None
+        else:
+            present, absent, values = make_workload(n, SEED)
+            d_keys = torch.from_numpy(present.view(np.int32)).to(device)
+            d_vals = torch.from_numpy(values.view(np.int32)).to(device)
+            d_abs = torch.from_numpy(absent.view(np.int32)).to(device)
         d_out = torch.empty(n, dtype=torch.int32, device=device)
         half = n // 2
         d_mixed = torch.cat([d_keys[:half], d_abs[:n - half]])[torch.randperm(n, device=device)].contiguous()
@@ -259,7 +267,7 @@ def run_cuda(args):
         outcome = table.last_insert_result()
         _, fs100 = table.find(d_keys, d_out, want_stats=True)
         assert fs100.hits == n
-        checksum_ok = fs100.value_sum == int(values.astype(np.uint64).sum())
+        checksum_ok = fs100.value_sum == int((d_vals.to(torch.int64) & 0xFFFFFFFF).sum().item())
         assert checksum_ok, "find checksum mismatch"
 
         def timed_find(q):
@@ -284,11 +292,13 @@ def run_cuda(args):
         find_bytes = bht.predict_sectors(KIND, B, fs100.mean_probes, bht.OP_FIND) * 32 * n
         dom_insert = ins_ms >= find_ms
         dom_bytes, dom_ms = (ins_bytes, ins_ms) if dom_insert else (find_bytes, find_ms)
-        roof = lambda by, ms: {"bound": "hbm", "achieved": by / (ms * 1e-3) / 1e9, "peak": peaks["hbm_gbs"],  # noqa: E731
-                               "unit": "GB/s", "frac": by / (ms * 1e-3) / 1e9 / peaks["hbm_gbs"], "traffic": None,
-                               "peak_source": peaks["source"]}
-        roofline = roof(dom_bytes, dom_ms)
-        roofline["kernel"] = "bulk_insert_cuckoo_kernel<16,3>" if dom_insert else "bulk_find_kernel<16,3,true>"
+        traffic = load_traffic() if n == N_KEYS else {}
+        roof = lambda by, ms, kern=None: {"bound": "hbm", "achieved": by / (ms * 1e-3) / 1e9, "peak": peaks["hbm_gbs"],  # noqa: E731
+                                          "unit": "GB/s", "frac": by / (ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
+                                          "traffic": traffic.get(kern), "peak_source": peaks["source"]}
+        dom_kernel = "bulk_insert_cuckoo_kernel<16,3>" if dom_insert else "bulk_find_kernel<16,3,true>"
+        roofline = roof(dom_bytes, dom_ms, dom_kernel)
+        roofline["kernel"] = dom_kernel
         roofline["algorithmic_bytes_per_key"] = dom_bytes / n
         roofline["frac_of_8TBps"] = dom_bytes / (dom_ms * 1e-3) / 8e12
         detail = {
@@ -297,14 +307,15 @@ def run_cuda(args):
             "find_50_mkeys": n / f50_ms / 1e3, "find_0_mkeys": n / f0_ms / 1e3,
             "insert_probes_per_key": outcome.mean_probes, "find_100_probes_per_key": fs100.mean_probes,
             "find_50_probes_per_key": fs50.mean_probes, "find_0_probes_per_key": fs0.mean_probes,
-            "roofline_insert": roof(ins_bytes, ins_ms), "roofline_find_100": roof(find_bytes, find_ms),
+            "roofline_insert": roof(ins_bytes, ins_ms, "bulk_insert_cuckoo_kernel<16,3>"),
+            "roofline_find_100": roof(find_bytes, find_ms, "bulk_find_kernel<16,3,true>"),
             "roofline_find_50": roof(bht.predict_sectors(KIND, B, fs50.mean_probes, bht.OP_FIND) * 32 * n, f50_ms),
             "roofline_find_0": roof(bht.predict_sectors(KIND, B, fs0.mean_probes, bht.OP_FIND) * 32 * n, f0_ms),
         }
 
         # ---- e2e: the same pass through the C ABI with HOST buffers (pinned), copies inside the timed region
-        h_keys = torch.from_numpy(present.view(np.int32)).pin_memory()
-        h_vals = torch.from_numpy(values.view(np.int32)).pin_memory()
+        h_keys = d_keys.cpu().pin_memory()
+        h_vals = d_vals.cpu().pin_memory()
         h_out = torch.empty(n, dtype=torch.int32).pin_memory()
         e2e_steps = max(2, min(args.steps, 5))
 
@@ -320,16 +331,17 @@ def run_cuda(args):
             o = e2e_step()
         torch.cuda.synchronize()
         e2e_s = (time.perf_counter() - t0) / e2e_steps
-        assert o.success and np.array_equal(h_out.numpy().view(np.uint32), values)
+        assert o.success and torch.equal(h_out, h_vals)
         e2e = {"value": 2 * n / e2e_s / 1e6, "unit": "MKeys/s", "h2d_bytes_per_step": 12 * n,
                "d2h_bytes_per_step": 4 * n + 64, "ms_per_step": e2e_s * 1e3,
                "api": "bht_insert / bht_find with BHT_MEM_HOST (pinned host arrays, 3-slot staged PCIe pipeline)"}
 
-        cpu = cpu_baseline_leg(args, present, n) if not args.no_cpu_baseline else None
+        cpu = cpu_baseline_leg(args, present, n) if not (args.no_cpu_baseline or args.device_keys) else None
         line = {
             "metric": METRIC, "value": value, "unit": "MKeys/s", "n_gpus": 1, "steps": args.steps,
             "warmup": max(args.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "u32/u64 integer", "data": "synthetic: unique uniform u32 keys, MT19937",
+            "vs_baseline": None, "dtype": "u32/u64 integer", "data": ("synthetic: unique u32 keys from the device bijection" if args.device_keys
+                                                    else "synthetic: unique uniform u32 keys, MT19937"),
             "config": wl, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clocks, "detail": detail,
         }
@@ -381,6 +393,15 @@ def run_cuda(args):
     return 0
 
 
+def load_traffic():
+    """DRAM bytes per launch of the two hot kernels from the committed `ncu --set full` capture of this very
+    workload (tools/ncu_summary.py --traffic-json); None when no capture has been committed."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(path):
+        return json.load(open(path))
+    return {}
+
+
 def load_peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(path):
@@ -418,6 +439,7 @@ def main():
     ap.add_argument("--keys", type=int, default=N_KEYS, help="keys per GPU")
     ap.add_argument("--chunk", type=int, default=1 << 24, help="sharded pipeline chunk (keys)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--device-keys", action="store_true", help="generate keys on the device (large --keys)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

@@ -48,6 +48,22 @@ def main():
                     keep = False
             if keep:
                 lines.append(f"{h:82s} {v:>18s} {units[i]}")
+    if "--traffic-json" in sys.argv:  # merge dram bytes per launch into profiles/traffic.json (read by bench.py)
+        import json, os, re
+        path = sys.argv[sys.argv.index("--traffic-json") + 1]
+        data = json.load(open(path)) if os.path.exists(path) else {}
+        for r in rows[2:]:
+            name = r[hdr.index("Kernel Name")]
+            m = re.match(r"(?:void )?(?:bht_b200::)?(\w+)<([^>]*)>", name)
+            key = f"{m.group(1)}<{m.group(2).replace(' ', '').replace('(int)', '').replace('(bool)', '')}>" if m else name
+            key = key.replace(",1>", ",true>").replace(",0>", ",false>") if key.startswith("bulk_find") else key
+
+            def val(metric):
+                v = float(r[hdr.index(metric)].replace(",", ""))
+                u = units[hdr.index(metric)]
+                return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[u]
+            data[key] = val("dram__bytes_read.sum") + val("dram__bytes_write.sum")
+        json.dump(data, open(path, "w"), indent=1)
     text = "\n".join(lines) + "\n"
     if out:
         open(out, "w").write(f"# ncu --set full --clock-control none summary of {rep}\n" + text)
