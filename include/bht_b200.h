@@ -179,6 +179,11 @@ bht_status bht_failed_keys(bht_table* table, uint32_t* host_out, uint64_t max_ke
 /* iht only: select the prose variant of iht_insert (table.cpp:167-169, `prose_fallback`). */
 bht_status bht_set_iht_prose_fallback(bht_table* table, int32_t enabled);
 
+/* Large device-resident inserts into a store much bigger than the L2 are routed by table region first
+ * (an L2-blocked build; same result set, different concurrent order).  mode 0 = never (caller order),
+ * 1 = when the sizes make it pay (default), 2 = always (small tables too; used by the parity tests). */
+bht_status bht_set_blocked_insert(bht_table* table, int32_t mode);
+
 /* ---- load factor / store access ---------------------------------------------------------- */
 
 /* realized_load() (table.hpp:40): inserted counter and capacity. */

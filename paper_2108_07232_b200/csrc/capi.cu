@@ -10,8 +10,10 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <new>
@@ -84,6 +86,9 @@ struct bht_table {
   DevCounters* ctr = nullptr;       // device
   DevCounters* ctr_host = nullptr;  // pinned mirror
   uint32_t* failed_keys = nullptr;  // device log of dropped keys
+  int blocked_insert = 1;  // 0 = caller order, 1 = routed when worth it, 2 = always routed (bht_set_blocked_insert)
+  uint32_t* cursors = nullptr;        // device: ring of per-launch work cursors (Stream, probe_engine.cuh)
+  std::atomic<uint32_t> cursor_seq{0};
   Staging stage;
   std::mutex mu;  // serialises calls that touch the counter block / staging buffers
 };
@@ -173,18 +178,72 @@ void fill_insert_result(const bht_table* t, uint64_t attempted, bht_insert_resul
   r->success = c.inserted == attempted ? 1u : 0u;
 }
 
-cudaError_t launch_insert_kind(const bht_table* t, const uint32_t* keys, const uint32_t* values, uint64_t n,
-                               cudaStream_t stream) {
+constexpr uint32_t kCursorSlots = 256;
+
+// A zeroed work cursor for one probe-kernel launch on `stream`.  Launches that may overlap (finds on different
+// streams) get different words of the ring.
+cudaError_t next_cursor(bht_table* t, cudaStream_t stream, uint32_t** out) {
+  *out = t->cursors + (t->cursor_seq.fetch_add(1, std::memory_order_relaxed) % kCursorSlots);
+  return cudaMemsetAsync(*out, 0, sizeof(uint32_t), stream);
+}
+
+cudaError_t launch_insert_kind(bht_table* t, PairSource src, uint64_t n, int max_ctas_per_sm, cudaStream_t stream) {
+  InsertLaunch a;
+  a.src = src;
+  a.n = n;
+  a.ctr = t->ctr;
+  a.failed_keys = t->failed_keys;
+  a.failed_cap = kFailedLogCap;
+  a.sm_count = t->sm_count;
+  a.max_ctas_per_sm = max_ctas_per_sm;
+  {
+    const char* e = std::getenv("BHT_DIRECT");  // experiment knob: 1 = direct engine everywhere, 2 = routed builds only
+    const int mode = e ? std::atoi(e) : 0;
+    a.direct = mode == 1 || (mode == 2 && src.values == nullptr);
+  }
+  a.stream = stream;
+  cudaError_t e = next_cursor(t, stream, &a.work_cursor);
+  if (e != cudaSuccess) return e;
+  {
+    const char* s = std::getenv("BHT_SWEEP_MB");  // tuning knob: L2 prefetch distance of a routed build, 0 = off
+    const long mb = s ? std::atol(s) : 16L;
+    t->view.sweep_ahead_bytes = static_cast<uint32_t>((mb < 0 ? 0 : (mb > 1024 ? 1024 : mb)) << 20);
+  }
   switch (t->cfg.kind) {
     case BHT_ONE_CHT:
     case BHT_BCHT:
-      return launch_insert_cuckoo(t->view, keys, values, n, t->ctr, t->failed_keys, kFailedLogCap, t->sm_count, stream);
+      return launch_insert_cuckoo(t->view, a);
     case BHT_BP2HT:
-      return launch_insert_p2(t->view, keys, values, n, t->ctr, t->failed_keys, kFailedLogCap, t->sm_count, stream);
+      return launch_insert_p2(t->view, a);
     case BHT_IHT:
-      return launch_insert_iht(t->view, keys, values, n, t->ctr, t->failed_keys, kFailedLogCap, t->sm_count, stream);
+      return launch_insert_iht(t->view, a);
     default: return cudaErrorInvalidValue;
   }
+}
+
+// Number of table regions for an L2-blocked insert of n device-resident pairs; 1 = insert in caller order.
+// Worth it only when the store is well beyond the L2 and the batch is large enough to amortise the routing
+// pass.  BHT_REGION_MB (environment) overrides the region size; 0 disables blocking.
+uint32_t blocked_regions(const bht_table* t, uint64_t n) {
+  const char* env = std::getenv("BHT_REGION_MB");
+  const long region_mb = env ? std::atol(env) : 32L;
+  if (region_mb <= 0 || t->blocked_insert == 0 || n > 0x7FFFFFFFull) return 1;
+  const uint64_t store_bytes = t->cfg.capacity * sizeof(uint64_t);
+  const bool forced = t->blocked_insert == 2;  // bht_set_blocked_insert(table, 2): route whatever the sizes (tests)
+  if (!forced && (n < (4ull << 20) || store_bytes < (192ull << 20))) return 1;
+  uint64_t r = (store_bytes + (static_cast<uint64_t>(region_mb) << 20) - 1) / (static_cast<uint64_t>(region_mb) << 20);
+  if (forced && r < 4) r = 4;
+  if (r > static_cast<uint64_t>(kMaxShards)) r = kMaxShards;
+  if (r >= t->cfg.num_buckets) r = t->cfg.num_buckets - 1;  // the router needs n_regions < hash range
+  return static_cast<uint32_t>(r < 2 ? 1 : r);
+}
+
+// Resident CTAs per SM of the insert kernel of a routed build: with the probes L2-resident a few hundred keys in
+// flight per SM saturate the path, and fewer keys in flight mean fewer lost slot races inside the region.
+// BHT_BLOCKED_CTAS (environment) overrides; 0 = whatever fits.
+int blocked_ctas_per_sm() {
+  const char* e = std::getenv("BHT_BLOCKED_CTAS");
+  return e ? std::atoi(e) : 0;
 }
 
 bool kind_matches(int32_t table_kind, int32_t as_kind) {
@@ -205,7 +264,23 @@ bht_status do_insert(bht_table* t, const uint32_t* keys, const uint32_t* values,
 
   BHT_CUDA(cudaMemsetAsync(t->ctr, 0, kPerCallCounterBytes, stream));
   if (mem_space == BHT_MEM_DEVICE) {
-    BHT_CUDA(launch_insert_kind(t, keys, values, n, stream));
+    const uint32_t regions = blocked_regions(t, n);
+    if (regions > 1) {
+      // L2-blocked build: group the pairs by the table region of their first bucket, then insert region by
+      // region, so that bucket fetches, claims and the write-back of dirty sectors happen while the region
+      // is L2-resident (the probe kernels deal their input out as one sliding window, probe_engine.cuh).
+      uint32_t* scratch = nullptr;  // n packed {key, value} pairs | counts | cursors | n destination bytes
+      BHT_CUDA(cudaMallocAsync(&scratch, 2 * n * sizeof(uint32_t) + 2 * regions * sizeof(unsigned long long) + n, stream));
+      unsigned long long* counts = reinterpret_cast<unsigned long long*>(scratch + 2 * n);
+      uint8_t* dest8 = reinterpret_cast<uint8_t*>(counts + 2 * regions);
+      cudaError_t e = launch_region_route(t->view.h[0], regions, keys, values, n, dest8, counts, counts + regions, scratch,
+                                          t->sm_count, stream);
+      if (e == cudaSuccess) e = launch_insert_kind(t, PairSource{scratch, nullptr}, n, blocked_ctas_per_sm(), stream);
+      cudaFreeAsync(scratch, stream);
+      if (e != cudaSuccess) return cuda_fail(e, "bht_insert (blocked)");
+    } else {
+      BHT_CUDA(launch_insert_kind(t, PairSource{keys, values}, n, 0, stream));
+    }
   } else if (n != 0) {
     bht_status s = ensure_staging(t);
     if (s != BHT_OK) return s;
@@ -223,7 +298,7 @@ bht_status do_insert(bht_table* t, const uint32_t* keys, const uint32_t* values,
       BHT_CUDA(cudaMemcpyAsync(st.vals[slot], values + off, len * sizeof(uint32_t), cudaMemcpyHostToDevice, st.h2d));
       BHT_CUDA(cudaEventRecord(st.in_done[slot], st.h2d));
       BHT_CUDA(cudaStreamWaitEvent(st.compute, st.in_done[slot], 0));
-      BHT_CUDA(launch_insert_kind(t, st.keys[slot], st.vals[slot], len, st.compute));
+      BHT_CUDA(launch_insert_kind(t, PairSource{st.keys[slot], st.vals[slot]}, len, 0, st.compute));
       BHT_CUDA(cudaEventRecord(st.kernel_done[slot], st.compute));
     }
     BHT_CUDA(cudaStreamWaitEvent(stream, st.kernel_done[(chunks - 1) % kStageSlots], 0));
@@ -248,7 +323,9 @@ bht_status do_find(const bht_table* ct, bool early_exit, const uint32_t* keys, u
 
   if (mem_space == BHT_MEM_DEVICE && result == nullptr) {
     // lock-free: concurrent finds on different streams share nothing but the read-only store
-    BHT_CUDA(launch_find(t->view, early_exit, keys, out, n, nullptr, t->sm_count, stream));
+    uint32_t* cursor = nullptr;
+    BHT_CUDA(next_cursor(t, stream, &cursor));
+    BHT_CUDA(launch_find(t->view, early_exit, keys, out, n, nullptr, cursor, t->sm_count, stream));
     return BHT_OK;
   }
 
@@ -256,7 +333,9 @@ bht_status do_find(const bht_table* ct, bool early_exit, const uint32_t* keys, u
   DevCounters* ctr = result != nullptr ? t->ctr : nullptr;
   if (ctr != nullptr) BHT_CUDA(cudaMemsetAsync(t->ctr, 0, kPerCallCounterBytes, stream));
   if (mem_space == BHT_MEM_DEVICE) {
-    BHT_CUDA(launch_find(t->view, early_exit, keys, out, n, ctr, t->sm_count, stream));
+    uint32_t* cursor = nullptr;
+    BHT_CUDA(next_cursor(t, stream, &cursor));
+    BHT_CUDA(launch_find(t->view, early_exit, keys, out, n, ctr, cursor, t->sm_count, stream));
   } else if (n != 0) {
     bht_status s = ensure_staging(t);
     if (s != BHT_OK) return s;
@@ -277,7 +356,9 @@ bht_status do_find(const bht_table* ct, bool early_exit, const uint32_t* keys, u
       BHT_CUDA(cudaMemcpyAsync(st.keys[slot], keys + off, len * sizeof(uint32_t), cudaMemcpyHostToDevice, st.h2d));
       BHT_CUDA(cudaEventRecord(st.in_done[slot], st.h2d));
       BHT_CUDA(cudaStreamWaitEvent(st.compute, st.in_done[slot], 0));
-      BHT_CUDA(launch_find(t->view, early_exit, st.keys[slot], st.vals[slot], len, ctr, t->sm_count, st.compute));
+      uint32_t* cursor = nullptr;
+      BHT_CUDA(next_cursor(t, st.compute, &cursor));
+      BHT_CUDA(launch_find(t->view, early_exit, st.keys[slot], st.vals[slot], len, ctr, cursor, t->sm_count, st.compute));
       BHT_CUDA(cudaEventRecord(st.kernel_done[slot], st.compute));
       BHT_CUDA(cudaStreamWaitEvent(st.d2h, st.kernel_done[slot], 0));
       BHT_CUDA(cudaMemcpyAsync(out + off, st.vals[slot], len * sizeof(uint32_t), cudaMemcpyDeviceToHost, st.d2h));
@@ -401,12 +482,22 @@ bht_status bht_create(const bht_config* cfg, int32_t device, bht_table** out) {
     return fail(BHT_CUDA_ERROR, "bht_create: kernels are built for sm_100a only; this device is older");
   }
   if (e == cudaSuccess) t->sm_count = prop.multiProcessorCount;
+  {
+    // scratch for routed inserts comes from the stream-ordered pool: keep it cached across calls instead of
+    // handing it back to the driver at every synchronisation
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      unsigned long long keep = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+  }
 
   uint64_t* store = nullptr;
   if (e == cudaSuccess) e = cudaMalloc(&store, cfg->capacity * sizeof(uint64_t));  // cudaMalloc aligns to >= 256 B
   if (e == cudaSuccess) e = cudaMalloc(&t->ctr, sizeof(DevCounters));
   if (e == cudaSuccess) e = cudaMallocHost(&t->ctr_host, sizeof(DevCounters));
   if (e == cudaSuccess) e = cudaMalloc(&t->failed_keys, kFailedLogCap * sizeof(uint32_t));
+  if (e == cudaSuccess) e = cudaMalloc(&t->cursors, kCursorSlots * sizeof(uint32_t));
   if (e == cudaSuccess) e = cudaMemset(t->ctr, 0, sizeof(DevCounters));
   if (e == cudaSuccess) e = launch_fill_empty(store, cfg->capacity, t->sm_count, nullptr);
   if (e == cudaSuccess) e = cudaStreamSynchronize(nullptr);
@@ -415,6 +506,7 @@ bht_status bht_create(const bht_config* cfg, int32_t device, bht_table** out) {
     if (t->ctr) cudaFree(t->ctr);
     if (t->ctr_host) cudaFreeHost(t->ctr_host);
     if (t->failed_keys) cudaFree(t->failed_keys);
+    if (t->cursors) cudaFree(t->cursors);
     delete t;
     return cuda_fail(e, "bht_create");
   }
@@ -431,6 +523,11 @@ bht_status bht_create(const bht_config* cfg, int32_t device, bht_table** out) {
   v.max_chain = cfg->max_chain;
   v.prose = 0;
   v.retry_cap = kRetryCap;
+  {
+    const char* e = std::getenv("BHT_CHUNK_LOG2");  // tuning knob: work-stream chunk (probe_engine.cuh, Stream)
+    const long c = e ? std::atol(e) : static_cast<long>(kDefaultChunkLog2);
+    v.chunk_log2 = static_cast<uint32_t>(c < 5 ? 5 : (c > 16 ? 16 : c));
+  }
   *out = t;
   return BHT_OK;
 }
@@ -444,6 +541,7 @@ bht_status bht_destroy(bht_table* t) {
   cudaFree(t->ctr);
   cudaFreeHost(t->ctr_host);
   cudaFree(t->failed_keys);
+  cudaFree(t->cursors);
   delete t;
   return BHT_OK;
 }
@@ -545,6 +643,13 @@ bht_status bht_set_iht_prose_fallback(bht_table* t, int32_t enabled) {
   if (t == nullptr) return fail(BHT_INVALID_ARGUMENT, "bht_set_iht_prose_fallback: null table");
   if (t->cfg.kind != BHT_IHT) return fail(BHT_KIND_MISMATCH, "iht_insert: table kind does not match the variant");
   t->view.prose = enabled ? 1u : 0u;
+  return BHT_OK;
+}
+
+bht_status bht_set_blocked_insert(bht_table* t, int32_t enabled) {
+  if (t == nullptr) return fail(BHT_INVALID_ARGUMENT, "bht_set_blocked_insert: null table");
+  if (enabled < 0 || enabled > 2) return fail(BHT_INVALID_ARGUMENT, "bht_set_blocked_insert: mode must be 0, 1 or 2");
+  t->blocked_insert = enabled;
   return BHT_OK;
 }
 
@@ -681,13 +786,12 @@ bht_status bht_shard_partition(uint64_t alpha, uint64_t beta, uint32_t n_shards,
   cudaDeviceProp prop;
   BHT_CUDA(cudaGetDeviceProperties(&prop, device));
   cudaStream_t s = as_stream(stream);
-  unsigned long long* scratch = nullptr;  // [counts | cursors]
-  BHT_CUDA(cudaMallocAsync(&scratch, 2 * sizeof(unsigned long long) * n_shards, s));
+  unsigned long long* scratch = nullptr;  // counts | cursors | n destination bytes
+  BHT_CUDA(cudaMallocAsync(&scratch, 2 * sizeof(unsigned long long) * n_shards + n, s));
   const uint32_t a = static_cast<uint32_t>(alpha), b = static_cast<uint32_t>(beta);
-  cudaError_t e = launch_shard_histogram(a, b, n_shards, keys, n, scratch, prop.multiProcessorCount, s);
-  if (e == cudaSuccess)
-    e = launch_shard_scatter(a, b, n_shards, keys, values, n, scratch, scratch + n_shards, out_keys, out_values, out_index,
-                             prop.multiProcessorCount, s);
+  cudaError_t e = launch_shard_route(a, b, n_shards, keys, values, n, reinterpret_cast<uint8_t*>(scratch + 2 * n_shards), scratch,
+                                     scratch + n_shards, out_keys, out_values,
+                                     out_index, prop.multiProcessorCount, s);
   if (e == cudaSuccess) e = cudaMemcpyAsync(counts_host, scratch, sizeof(uint64_t) * n_shards, cudaMemcpyDeviceToHost, s);
   cudaFreeAsync(scratch, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);

@@ -19,36 +19,47 @@ namespace bht_b200 {
 template <int B, int H, bool EARLY_EXIT>
 __global__ void __launch_bounds__(block_threads<B>(1))
 bulk_find_kernel(const __grid_constant__ TableView t, const uint32_t* __restrict__ keys, uint32_t* __restrict__ out,
-                 uint64_t n, DevCounters* __restrict__ ctr) {
+                 uint64_t n, DevCounters* __restrict__ ctr, uint32_t* __restrict__ work_cursor) {
   using G = Geo<B>;
   extern __shared__ __align__(1024) unsigned char smem[];
   const int lane = threadIdx.x & 31;
   const uint32_t stage = smem_u32(smem) + (threadIdx.x >> 5) * G::WARP_BYTES;
   const uint32_t lt_mask = (1u << lane) - 1u;
 
-  Stream st = warp_stream(n);
+  Stream st;
+  st.init(n, t.chunk_log2, work_cursor, lane);
   uint32_t probes = 0, hits = 0;
   unsigned long long vsum = 0;
 
   bool have = false;
   uint32_t key = 0, round = 0;
   uint64_t idx = 0;
-  uint32_t ahead = lane < st.len ? __ldg(keys + st.at(lane)) : 0u;  // next 32 keys of the stream
+  // the next 32 queries of the stream, one per lane, and how many of them exist
+  uint32_t ahead, ahead_n;
+  {
+    uint64_t g;
+    const bool in = st.index(lane, t.chunk_log2, g);
+    ahead = in ? __ldcs(keys + g) : 0u;
+    ahead_n = __popc(__ballot_sync(kFullMask, in));
+  }
 
   for (;;) {
     // ---- refill: idle lanes take the next unread queries, in order
     const uint32_t idle = __ballot_sync(kFullMask, !have);
-    if (idle != 0 && st.cursor < st.len) {
+    if (idle != 0 && ahead_n != 0) {
       const uint32_t rank = __popc(idle & lt_mask);
       const uint32_t fresh = __shfl_sync(kFullMask, ahead, rank);
-      if (!have && st.cursor + rank < st.len) {
+      if (!have && rank < ahead_n) {
         key = fresh;
-        idx = st.at(st.cursor + rank);
+        st.index(rank, t.chunk_log2, idx);
         round = 0;
         have = true;
       }
-      st.cursor = min(st.cursor + __popc(idle), st.len);
-      ahead = st.cursor + lane < st.len ? __ldg(keys + st.at(st.cursor + lane)) : 0u;
+      st.advance(min(static_cast<uint32_t>(__popc(idle)), ahead_n), t.chunk_log2, work_cursor, lane);
+      uint64_t g;
+      const bool in = st.index(lane, t.chunk_log2, g);
+      ahead = in ? __ldcs(keys + g) : 0u;
+      ahead_n = __popc(__ballot_sync(kFullMask, in));
     }
     if (!__any_sync(kFullMask, have)) break;
 
@@ -76,7 +87,7 @@ bulk_find_kernel(const __grid_constant__ TableView t, const uint32_t* __restrict
         }
       }
       if (done) {
-        out[idx] = answer;
+        __stcs(out + idx, answer);
         have = false;
       }
     }
@@ -95,44 +106,44 @@ bulk_find_kernel(const __grid_constant__ TableView t, const uint32_t* __restrict
 
 template <int B, int H, bool EARLY_EXIT>
 static cudaError_t launch_one(const TableView& t, const uint32_t* keys, uint32_t* out, uint64_t n, DevCounters* ctr,
-                              int sm_count, cudaStream_t stream) {
+                              uint32_t* work_cursor, int sm_count, cudaStream_t stream) {
   auto kernel = bulk_find_kernel<B, H, EARLY_EXIT>;
   constexpr int block = block_threads<B>(1);
   constexpr int smem = (block / 32) * Geo<B>::WARP_BYTES;
   const int grid = persistent_grid(kernel, block, smem, sm_count, n, block);
-  kernel<<<grid, block, smem, stream>>>(t, keys, out, n, ctr);
+  kernel<<<grid, block, smem, stream>>>(t, keys, out, n, ctr, work_cursor);
   note_launch();
   return cudaGetLastError();
 }
 
 template <int B>
 static cudaError_t launch_b(const TableView& t, bool early_exit, const uint32_t* keys, uint32_t* out, uint64_t n,
-                            DevCounters* ctr, int sm_count, cudaStream_t stream) {
+                            DevCounters* ctr, uint32_t* work_cursor, int sm_count, cudaStream_t stream) {
   switch (t.n_hashes) {
-    case 2: return launch_one<B, 2, false>(t, keys, out, n, ctr, sm_count, stream);
+    case 2: return launch_one<B, 2, false>(t, keys, out, n, ctr, work_cursor, sm_count, stream);
     case 3:
-      return early_exit ? launch_one<B, 3, true>(t, keys, out, n, ctr, sm_count, stream)
-                        : launch_one<B, 3, false>(t, keys, out, n, ctr, sm_count, stream);
+      return early_exit ? launch_one<B, 3, true>(t, keys, out, n, ctr, work_cursor, sm_count, stream)
+                        : launch_one<B, 3, false>(t, keys, out, n, ctr, work_cursor, sm_count, stream);
     case 4:
       if constexpr (B == 1)
-        return early_exit ? launch_one<1, 4, true>(t, keys, out, n, ctr, sm_count, stream)
-                          : launch_one<1, 4, false>(t, keys, out, n, ctr, sm_count, stream);
+        return early_exit ? launch_one<1, 4, true>(t, keys, out, n, ctr, work_cursor, sm_count, stream)
+                          : launch_one<1, 4, false>(t, keys, out, n, ctr, work_cursor, sm_count, stream);
       return cudaErrorInvalidValue;
     default: return cudaErrorInvalidValue;
   }
 }
 
 cudaError_t launch_find(const TableView& t, bool early_exit, const uint32_t* keys, uint32_t* out, uint64_t n,
-                        DevCounters* ctr, int sm_count, cudaStream_t stream) {
+                        DevCounters* ctr, uint32_t* work_cursor, int sm_count, cudaStream_t stream) {
   if (n == 0) return cudaSuccess;
   switch (t.bucket_size) {
-    case 1: return launch_b<1>(t, early_exit, keys, out, n, ctr, sm_count, stream);
-    case 2: return launch_b<2>(t, early_exit, keys, out, n, ctr, sm_count, stream);
-    case 4: return launch_b<4>(t, early_exit, keys, out, n, ctr, sm_count, stream);
-    case 8: return launch_b<8>(t, early_exit, keys, out, n, ctr, sm_count, stream);
-    case 16: return launch_b<16>(t, early_exit, keys, out, n, ctr, sm_count, stream);
-    case 32: return launch_b<32>(t, early_exit, keys, out, n, ctr, sm_count, stream);
-    case 64: return launch_b<64>(t, early_exit, keys, out, n, ctr, sm_count, stream);
+    case 1: return launch_b<1>(t, early_exit, keys, out, n, ctr, work_cursor, sm_count, stream);
+    case 2: return launch_b<2>(t, early_exit, keys, out, n, ctr, work_cursor, sm_count, stream);
+    case 4: return launch_b<4>(t, early_exit, keys, out, n, ctr, work_cursor, sm_count, stream);
+    case 8: return launch_b<8>(t, early_exit, keys, out, n, ctr, work_cursor, sm_count, stream);
+    case 16: return launch_b<16>(t, early_exit, keys, out, n, ctr, work_cursor, sm_count, stream);
+    case 32: return launch_b<32>(t, early_exit, keys, out, n, ctr, work_cursor, sm_count, stream);
+    case 64: return launch_b<64>(t, early_exit, keys, out, n, ctr, work_cursor, sm_count, stream);
     default: return cudaErrorInvalidValue;
   }
 }

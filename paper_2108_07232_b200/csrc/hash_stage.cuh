@@ -88,6 +88,16 @@ __host__ __device__ __forceinline__ uint32_t xorshift_next_below(uint64_t& state
   return static_cast<uint32_t>(((x >> 32) * bound) >> 32);
 }
 
+// next_below for the lanes that draw (`draw`); the others keep their state and get 0.
+__host__ __device__ __forceinline__ uint32_t xorshift_next_below_if(uint64_t& state, uint32_t bound, bool draw) {
+  uint64_t x = state;
+  x ^= x << 13;
+  x ^= x >> 7;
+  x ^= x << 17;
+  state = draw ? x : state;
+  return draw ? static_cast<uint32_t>(((x >> 32) * bound) >> 32) : 0u;
+}
+
 // Synthetic workload (bht_generate_unique_keys): a keyed bijection of the 32-bit counter, every step
 // invertible mod 2^32, cycle-walked once past the sentinel so that counters [0, 2^32-2] map one-to-one
 // onto user keys [0, 2^32-2] (the key universe of core.hpp:23-24) without keygen.cpp's rejection set.

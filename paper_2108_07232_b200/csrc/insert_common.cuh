@@ -25,41 +25,49 @@ __device__ __forceinline__ void flush_insert_counters(DevCounters* ctr, int lane
   }
 }
 
-// The (key, value) stream of one warp: the next 32 pairs of the warp's slice are prefetched one
+// The (key, value) stream of one warp: the next 32 pairs of the warp's stream are prefetched one
 // round ahead; idle lanes take them in order.
 struct PairFeed {
   Stream st;
-  const uint32_t* keys;
-  const uint32_t* values;
   uint32_t ahead_k, ahead_v;
+  uint32_t ahead_n;  // how many of the 32 prefetched pairs exist (warp-uniform)
 
-  __device__ __forceinline__ void init(const uint32_t* __restrict__ k, const uint32_t* __restrict__ v, uint64_t n, int lane) {
-    st = warp_stream(n);
-    keys = k;
-    values = v;
-    prefetch(lane);
+  // src / shift / cursor are kernel parameters: passed at every call rather than kept in registers
+  __device__ __forceinline__ void init(const PairSource& src, uint64_t n, uint32_t shift, uint32_t* cursor, int lane) {
+    st.init(n, shift, cursor, lane);
+    prefetch(src, shift, lane);
   }
-  __device__ __forceinline__ void prefetch(int lane) {
-    const uint32_t p = st.cursor + lane;
-    const bool in = p < st.len;
-    const uint64_t g = st.at(p);
-    ahead_k = in ? __ldg(keys + g) : 0u;
-    ahead_v = in ? __ldg(values + g) : 0u;
+  __device__ __forceinline__ void prefetch(const PairSource& src, uint32_t shift, int lane) {
+    uint64_t g;
+    const bool in = st.index(lane, shift, g);
+    ahead_k = ahead_v = 0u;
+    if (in) {
+      if (src.values == nullptr) {  // kernel-uniform
+        const uint2 kv = __ldcs(reinterpret_cast<const uint2*>(src.keys) + g);
+        ahead_k = kv.x;
+        ahead_v = kv.y;
+      } else {
+        ahead_k = __ldcs(src.keys + g);
+        ahead_v = __ldcs(src.values + g);
+      }
+    }
+    ahead_n = __popc(__ballot_sync(kFullMask, in));
   }
   // Returns true for lanes that received a fresh pair.
-  __device__ __forceinline__ bool refill(bool have, int lane, uint32_t& key, uint32_t& val) {
+  __device__ __forceinline__ bool refill(const PairSource& src, uint32_t shift, uint32_t* cursor, bool have, int lane,
+                                         uint32_t& key, uint32_t& val) {
     const uint32_t idle = __ballot_sync(kFullMask, !have);
-    if (idle == 0 || st.cursor >= st.len) return false;
+    if (idle == 0 || ahead_n == 0) return false;
     const uint32_t rank = __popc(idle & ((1u << lane) - 1u));
     const uint32_t fk = __shfl_sync(kFullMask, ahead_k, rank);
     const uint32_t fv = __shfl_sync(kFullMask, ahead_v, rank);
-    const bool got = !have && st.cursor + rank < st.len;
+    const bool got = !have && rank < ahead_n;
     if (got) {
       key = fk;
       val = fv;
     }
-    st.cursor = min(st.cursor + __popc(idle), st.len);
-    prefetch(lane);
+    st.advance(min(static_cast<uint32_t>(__popc(idle)), ahead_n), shift, cursor, lane);
+    prefetch(src, shift, lane);
     return got;
   }
 };

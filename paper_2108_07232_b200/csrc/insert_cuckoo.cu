@@ -23,56 +23,111 @@
 
 namespace bht_b200 {
 
-template <int B, int H>
-__global__ void __launch_bounds__(block_threads<B>(1))
-bulk_insert_cuckoo_kernel(const __grid_constant__ TableView t, const uint32_t* __restrict__ keys,
-                          const uint32_t* __restrict__ values, uint64_t n, DevCounters* __restrict__ ctr,
-                          uint32_t* __restrict__ failed_keys, uint64_t failed_cap) {
+// DIRECT selects the register-resident probe (direct_load) instead of the shared-memory staged one.
+template <int B, int H, bool DIRECT>
+__global__ void __launch_bounds__(block_threads<B>(1), DIRECT ? 3 : 6)
+bulk_insert_cuckoo_kernel(const __grid_constant__ TableView t, const PairSource src, uint64_t n,
+                          DevCounters* __restrict__ ctr, uint32_t* __restrict__ failed_keys, uint64_t failed_cap,
+                          uint32_t* __restrict__ work_cursor) {
   using G = Geo<B>;
   extern __shared__ __align__(1024) unsigned char smem[];
   const int lane = threadIdx.x & 31;
-  const uint32_t stage = smem_u32(smem) + (threadIdx.x >> 5) * G::WARP_BYTES;
+  const uint32_t stage = DIRECT ? 0u : smem_u32(smem) + (threadIdx.x >> 5) * G::WARP_BYTES;
   unsigned long long* store = reinterpret_cast<unsigned long long*>(t.store);
 
   uint64_t rng = xorshift_init(mix_seed(t.seed, 0x65766963ull + static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x));
   uint32_t n_ins = 0, n_fail = 0, n_probe = 0;
 
   PairFeed feed;
-  feed.init(keys, values, n, lane);
+  feed.init(src, n, t.chunk_log2, work_cursor, lane);
   bool have = false;
   uint32_t key = 0, val = 0, bid = 0, chain = 0, retries = 0;
+  // A lost CAS at slot L proves that slot L is taken now, and occupied slots form a prefix (probe_engine.cuh):
+  // the re-snapshot of the reference loop (table.cpp:89) can only report a load > L, so the lane goes straight
+  // for slot L + 1 next round without reading the bucket again (`hint`; B = "the bucket is full").
+  constexpr uint32_t kNoHint = 0xFFFFFFFFu;
+  constexpr uint32_t kSitOut = 0xFFFFFFFEu;  // routed builds: the lane's next bucket is being prefetched into L2
+  uint32_t hint = kNoHint;
+
+  // Routed (L2-blocked) build: the pairs arrive grouped by table region in table order, so input position and
+  // table position advance together.  (1) A sequential sweep runs `kSweepAhead` of the table ahead of the
+  // window: whenever the warp starts a chunk it prefetches the matching slice of the store into L2, so first
+  // touches of a bucket are L2 hits.  (2) A bucket outside the region (the next bucket of an evicted pair) is
+  // prefetched as soon as it is known and the lane sits one round out; it reads the line when it has arrived.
+  // Every round of a warp then waits for L2, not for the slowest HBM access among its 32 lanes.
+  const bool routed = src.values == nullptr;  // kernel-uniform
+  const uint32_t lines_per_bucket = (B * 8 + 127) / 128;
+  const uint64_t n_lines = (t.num_buckets * B * 8 + 127) / 128;
+  uint32_t swept_chunk = 0xFFFFFFFFu;
+  if (routed) {  // cold start: the first `sweep_ahead_bytes` of the store
+    const uint64_t ahead = min(static_cast<uint64_t>(t.sweep_ahead_bytes) >> 7, n_lines);
+    const uint64_t warp = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    for (uint64_t l = warp * 32 + lane; l < ahead; l += static_cast<uint64_t>(Stream::grid_warps()) * 32)
+      prefetch_l2(reinterpret_cast<const char*>(t.store) + (l << 7));
+  }
 
   for (;;) {
-    if (feed.refill(have, lane, key, val)) {
+    if (feed.refill(src, t.chunk_log2, work_cursor, have, lane, key, val)) {
       have = true;
       bid = bucket_index(t.h[0], key);
       chain = 0;
       retries = 0;
+      hint = kNoHint;
     }
     if (!__any_sync(kFullMask, have)) break;
+    if (routed && feed.st.cur != swept_chunk && feed.st.cur < feed.st.n_chunks) {  // warp-uniform
+      swept_chunk = feed.st.cur;
+      // the slice of this chunk: lines [c * L / n_chunks, (c + 1) * L / n_chunks), shifted ahead
+      const uint64_t first = static_cast<uint64_t>(swept_chunk) * n_lines / feed.st.n_chunks;
+      const uint64_t last = (static_cast<uint64_t>(swept_chunk) + 1) * n_lines / feed.st.n_chunks;
+      const uint64_t ahead = (static_cast<uint64_t>(t.sweep_ahead_bytes) >> 7);
+      for (uint64_t l = first + lane; l < last; l += 32)
+        if (l + ahead < n_lines) prefetch_l2(reinterpret_cast<const char*>(t.store) + ((l + ahead) << 7));
+    }
 
-    fetch_issue<B>(stage, t.store, have ? bid : kNoBucket, lane);
-    if (G::STAGED) fetch_wait();
+    const bool sitting = have && hint == kSitOut;
+    const bool snapshot = have && hint == kNoHint;
+    uint32_t load = hint;
+    if constexpr (DIRECT) {
+      const uint32_t l = direct_load<B>(t.store, snapshot ? bid : kNoBucket, lane);
+      if (snapshot) load = l;
+    } else {
+      fetch_issue<B>(stage, t.store, snapshot ? bid : kNoBucket, lane);
+      if (G::STAGED) fetch_wait();
+      if (snapshot) load = scan_bucket<B, false>(stage, t.store, bid, key, lane).load;
+    }
+    n_probe += snapshot;
+    hint = kNoHint;
+    // Decide first, then issue the lane's one atomic, then look at the results: the claims (CAS) and the
+    // evictions (EXCH) of a round are all in flight together instead of one divergent path after the other.
+    const bool claim = have && !sitting && load < B;
+    const bool dropped = have && !sitting && !claim && chain == t.max_chain;  // cap checked BEFORE the exchange (table.cpp:67)
+    const bool evict = have && !sitting && !claim && !dropped;
+    const uint32_t slot = claim ? load : xorshift_next_below_if(rng, B, evict);
+    unsigned long long* target = store + static_cast<uint64_t>(bid) * B + slot;
+    const unsigned long long pair = pack_pair(key, val);
+    unsigned long long got_c = 0, got_e = 0;  // separate registers: no write-after-write wait between the two
+    if (claim) got_c = atomicCAS(target, kEmptySlot, pair);
+    if (evict) got_e = atomicExch(target, pair);
+    __syncwarp();  // every row is scanned (the next round may overwrite it) and both kinds of atomics are issued
     if (have) {
-      const Scan s = scan_bucket<B, false>(stage, t.store, bid, key, lane);
-      ++n_probe;
-      unsigned long long* bucket = store + static_cast<uint64_t>(bid) * B;
-      if (s.load < B) {
-        if (atomicCAS(bucket + s.load, kEmptySlot, pack_pair(key, val)) == kEmptySlot) {
+      if (claim) {
+        if (got_c == kEmptySlot) {
           ++n_ins;
           have = false;
-        } else if (++retries > t.retry_cap) {  // lost the slot; re-snapshot the same bucket next round
+        } else if (++retries > t.retry_cap) {
           ++n_fail;
           record_failed(ctr, failed_keys, failed_cap, key);
           have = false;
+        } else {
+          hint = load + 1;  // lost the slot
         }
-      } else if (chain == t.max_chain) {
+      } else if (dropped) {
         ++n_fail;
         record_failed(ctr, failed_keys, failed_cap, key);  // the pair in hand is the one dropped
         have = false;
-      } else {
-        const unsigned long long old = atomicExch(bucket + xorshift_next_below(rng, B), pack_pair(key, val));
-        const uint32_t vk = static_cast<uint32_t>(old);
+      } else if (evict) {
+        const uint32_t vk = static_cast<uint32_t>(got_e);
         if (vk == kEmptyKey) {  // exchanged into a hole: only possible on an uploaded store
           ++n_ins;
           have = false;
@@ -85,41 +140,52 @@ bulk_insert_cuckoo_kernel(const __grid_constant__ TableView t, const uint32_t* _
           for (int i = H - 1; i >= 0; --i)  // lowest matching index wins (table.cpp:74-80)
             if (cand[i] == bid) next = cand[(i + 1) % H];
           key = vk;
-          val = static_cast<uint32_t>(old >> 32);
+          val = static_cast<uint32_t>(got_e >> 32);
           bid = next;
           ++chain;
+          if (routed) {  // most likely outside the region: fetch it into L2 now, read it the round after next
+#pragma unroll
+            for (uint32_t l = 0; l < lines_per_bucket; ++l)
+              prefetch_l2(reinterpret_cast<const char*>(t.store + static_cast<uint64_t>(bid) * B) + l * 128);
+            hint = kSitOut;
+          }
         }
       }
     }
-    if (G::STAGED) __syncwarp();
   }
 
   flush_insert_counters(ctr, lane, n_ins, n_fail, n_probe);
 }
 
 template <int B, int H>
-static cudaError_t launch_one(const TableView& t, const uint32_t* keys, const uint32_t* values, uint64_t n,
-                              DevCounters* ctr, uint32_t* failed_keys, uint64_t failed_cap, int sm_count,
-                              cudaStream_t stream) {
-  auto kernel = bulk_insert_cuckoo_kernel<B, H>;
+static cudaError_t launch_one(const TableView& t, const InsertLaunch& a) {
+  if constexpr (B >= 4 && B <= 16) {
+    if (a.direct) {
+      auto kernel = bulk_insert_cuckoo_kernel<B, H, true>;
+      constexpr int block = block_threads<B>(1);
+      const int grid = persistent_grid(kernel, block, 0, a.sm_count, a.n, block, a.max_ctas_per_sm);
+      kernel<<<grid, block, 0, a.stream>>>(t, a.src, a.n, a.ctr, a.failed_keys, a.failed_cap, a.work_cursor);
+      note_launch();
+      return cudaGetLastError();
+    }
+  }
+  auto kernel = bulk_insert_cuckoo_kernel<B, H, false>;
   constexpr int block = block_threads<B>(1);
   constexpr int smem = (block / 32) * Geo<B>::WARP_BYTES;
-  const int grid = persistent_grid(kernel, block, smem, sm_count, n, block);
-  kernel<<<grid, block, smem, stream>>>(t, keys, values, n, ctr, failed_keys, failed_cap);
+  const int grid = persistent_grid(kernel, block, smem, a.sm_count, a.n, block, a.max_ctas_per_sm);
+  kernel<<<grid, block, smem, a.stream>>>(t, a.src, a.n, a.ctr, a.failed_keys, a.failed_cap, a.work_cursor);
   note_launch();
   return cudaGetLastError();
 }
 
-cudaError_t launch_insert_cuckoo(const TableView& t, const uint32_t* keys, const uint32_t* values, uint64_t n,
-                                 DevCounters* ctr, uint32_t* failed_keys, uint64_t failed_cap, int sm_count,
-                                 cudaStream_t stream) {
-  if (n == 0) return cudaSuccess;
+cudaError_t launch_insert_cuckoo(const TableView& t, const InsertLaunch& a) {
+  if (a.n == 0) return cudaSuccess;
   if (t.n_hashes == 4) {
     if (t.bucket_size != 1) return cudaErrorInvalidValue;
-    return launch_one<1, 4>(t, keys, values, n, ctr, failed_keys, failed_cap, sm_count, stream);
+    return launch_one<1, 4>(t, a);
   }
   if (t.n_hashes != 3) return cudaErrorInvalidValue;
-#define CALL(BB) launch_one<BB, 3>(t, keys, values, n, ctr, failed_keys, failed_cap, sm_count, stream)
+#define CALL(BB) launch_one<BB, 3>(t, a)
   BHT_DISPATCH_BUCKET_SIZE(t.bucket_size, CALL)
 #undef CALL
 }

@@ -17,9 +17,9 @@ namespace bht_b200 {
 
 template <int B>
 __global__ void __launch_bounds__(block_threads<B>(2))
-bulk_insert_iht_kernel(const __grid_constant__ TableView t, const uint32_t* __restrict__ keys,
-                       const uint32_t* __restrict__ values, uint64_t n, DevCounters* __restrict__ ctr,
-                       uint32_t* __restrict__ failed_keys, uint64_t failed_cap) {
+bulk_insert_iht_kernel(const __grid_constant__ TableView t, const PairSource src, uint64_t n,
+                       DevCounters* __restrict__ ctr, uint32_t* __restrict__ failed_keys, uint64_t failed_cap,
+                       uint32_t* __restrict__ work_cursor) {
   using G = Geo<B>;
   extern __shared__ __align__(1024) unsigned char smem[];
   const int lane = threadIdx.x & 31;
@@ -29,12 +29,12 @@ bulk_insert_iht_kernel(const __grid_constant__ TableView t, const uint32_t* __re
   uint32_t n_ins = 0, n_fail = 0, n_probe = 0;
 
   PairFeed feed;
-  feed.init(keys, values, n, lane);
+  feed.init(src, n, t.chunk_log2, work_cursor, lane);
   bool have = false, overflow = false;  // overflow: phase 1 (primary already read, at or past t)
   uint32_t key = 0, val = 0, pb = 0, pl = 0, s0 = 0, s1 = 0, retries = 0;
 
   for (;;) {
-    if (feed.refill(have, lane, key, val)) {
+    if (feed.refill(src, t.chunk_log2, work_cursor, have, lane, key, val)) {
       have = true;
       overflow = false;
       pb = bucket_index(t.h[0], key);
@@ -95,24 +95,20 @@ bulk_insert_iht_kernel(const __grid_constant__ TableView t, const uint32_t* __re
 }
 
 template <int B>
-static cudaError_t launch_one(const TableView& t, const uint32_t* keys, const uint32_t* values, uint64_t n,
-                              DevCounters* ctr, uint32_t* failed_keys, uint64_t failed_cap, int sm_count,
-                              cudaStream_t stream) {
+static cudaError_t launch_one(const TableView& t, const InsertLaunch& a) {
   auto kernel = bulk_insert_iht_kernel<B>;
   constexpr int block = block_threads<B>(2);
   constexpr int smem = (block / 32) * 2 * Geo<B>::WARP_BYTES;
-  const int grid = persistent_grid(kernel, block, smem, sm_count, n, block);
-  kernel<<<grid, block, smem, stream>>>(t, keys, values, n, ctr, failed_keys, failed_cap);
+  const int grid = persistent_grid(kernel, block, smem, a.sm_count, a.n, block, a.max_ctas_per_sm);
+  kernel<<<grid, block, smem, a.stream>>>(t, a.src, a.n, a.ctr, a.failed_keys, a.failed_cap, a.work_cursor);
   note_launch();
   return cudaGetLastError();
 }
 
-cudaError_t launch_insert_iht(const TableView& t, const uint32_t* keys, const uint32_t* values, uint64_t n,
-                              DevCounters* ctr, uint32_t* failed_keys, uint64_t failed_cap, int sm_count,
-                              cudaStream_t stream) {
-  if (n == 0) return cudaSuccess;
+cudaError_t launch_insert_iht(const TableView& t, const InsertLaunch& a) {
+  if (a.n == 0) return cudaSuccess;
   if (t.n_hashes != 3) return cudaErrorInvalidValue;
-#define CALL(BB) launch_one<BB>(t, keys, values, n, ctr, failed_keys, failed_cap, sm_count, stream)
+#define CALL(BB) launch_one<BB>(t, a)
   BHT_DISPATCH_BUCKET_SIZE(t.bucket_size, CALL)
 #undef CALL
 }

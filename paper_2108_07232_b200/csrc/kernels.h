@@ -11,18 +11,32 @@ namespace bht_b200 {
 // find.cu — K3 bulk_find<kind, b>.  early_exit selects bcht_find's non-full early exit
 // (table.cpp:104); without it the same kernel is bp2ht_find / iht_find / bcht_find_no_early_exit.
 cudaError_t launch_find(const TableView& t, bool early_exit, const uint32_t* keys, uint32_t* out, uint64_t n,
-                        DevCounters* ctr, int sm_count, cudaStream_t stream);
+                        DevCounters* ctr, uint32_t* work_cursor, int sm_count, cudaStream_t stream);
+
+// Input of the bulk inserts: two arrays (the caller's keys / values) or one array of packed pairs
+// {key, value} (what the region router writes for an L2-blocked build).  Read once: streaming loads.
+struct PairSource {
+  const uint32_t* keys;
+  const uint32_t* values;  // null: `keys` holds packed pairs
+};
+
+struct InsertLaunch {
+  PairSource src;
+  uint64_t n;
+  DevCounters* ctr;
+  uint32_t* failed_keys;  // dropped-key log and its capacity
+  uint64_t failed_cap;
+  uint32_t* work_cursor;  // one zeroed device word per launch (Stream)
+  int sm_count;
+  int max_ctas_per_sm;    // 0 = whatever fits; a routed (L2-blocked) build keeps fewer keys in flight
+  bool direct;            // cuckoo, 4 <= b <= 16: register-resident probe (direct_load) instead of the staged one
+  cudaStream_t stream;
+};
 
 // insert_cuckoo.cu — K4 (bcht, 1cht); insert_p2.cu — K5 (bp2ht); insert_iht.cu — K6 (iht).
-cudaError_t launch_insert_cuckoo(const TableView& t, const uint32_t* keys, const uint32_t* values, uint64_t n,
-                                 DevCounters* ctr, uint32_t* failed_keys, uint64_t failed_cap, int sm_count,
-                                 cudaStream_t stream);
-cudaError_t launch_insert_p2(const TableView& t, const uint32_t* keys, const uint32_t* values, uint64_t n,
-                             DevCounters* ctr, uint32_t* failed_keys, uint64_t failed_cap, int sm_count,
-                             cudaStream_t stream);
-cudaError_t launch_insert_iht(const TableView& t, const uint32_t* keys, const uint32_t* values, uint64_t n,
-                              DevCounters* ctr, uint32_t* failed_keys, uint64_t failed_cap, int sm_count,
-                              cudaStream_t stream);
+cudaError_t launch_insert_cuckoo(const TableView& t, const InsertLaunch& a);
+cudaError_t launch_insert_p2(const TableView& t, const InsertLaunch& a);
+cudaError_t launch_insert_iht(const TableView& t, const InsertLaunch& a);
 
 // util.cu — K0 fill, K7 count, admissibility, hash hook, K8/K9 shard routing, synthetic keys.
 cudaError_t launch_fill_empty(uint64_t* store, uint64_t n_slots, int sm_count, cudaStream_t stream);
@@ -32,12 +46,16 @@ cudaError_t launch_count_inadmissible(const TableView& t, unsigned long long* ou
 cudaError_t launch_hash_keys(const HashFn& h, const uint32_t* keys, uint32_t* out, uint64_t n, int sm_count,
                              cudaStream_t stream);
 constexpr int kMaxShards = 256;
-cudaError_t launch_shard_histogram(uint32_t alpha, uint32_t beta, uint32_t n_shards, const uint32_t* keys, uint64_t n,
-                                   unsigned long long* counts, int sm_count, cudaStream_t stream);
-cudaError_t launch_shard_scatter(uint32_t alpha, uint32_t beta, uint32_t n_shards, const uint32_t* keys,
-                                 const uint32_t* values, uint64_t n, const unsigned long long* counts,
-                                 unsigned long long* cursors, uint32_t* out_keys, uint32_t* out_values,
-                                 uint32_t* out_index, int sm_count, cudaStream_t stream);
+// counts / cursors: n_dest device words each; scratch8: n bytes (4-byte aligned) for the per-key destinations.
+// out_* receive the elements grouped by destination.
+cudaError_t launch_shard_route(uint32_t alpha, uint32_t beta, uint32_t n_shards, const uint32_t* keys, const uint32_t* values,
+                               uint64_t n, uint8_t* scratch8, unsigned long long* counts, unsigned long long* cursors,
+                               uint32_t* out_keys, uint32_t* out_values, uint32_t* out_index, int sm_count, cudaStream_t stream);
+// Groups pairs by the table region (n_regions contiguous ranges of buckets) of their first bucket; out_pairs
+// receives n packed {key, value} pairs (8 bytes each).
+cudaError_t launch_region_route(const HashFn& h0, uint32_t n_regions, const uint32_t* keys, const uint32_t* values, uint64_t n,
+                                uint8_t* scratch8, unsigned long long* counts, unsigned long long* cursors, uint32_t* out_pairs,
+                                int sm_count, cudaStream_t stream);
 cudaError_t launch_unpermute(const uint32_t* answers, const uint32_t* index, uint64_t n, uint32_t* out, int sm_count,
                              cudaStream_t stream);
 cudaError_t launch_generate_keys(uint64_t seed, uint64_t offset, uint64_t n, uint32_t* keys, uint32_t* values,
@@ -51,9 +69,10 @@ uint64_t launch_count();
 // more than the work.
 template <typename Kernel>
 inline int persistent_grid(Kernel kernel, int block, int smem, int sm_count, uint64_t work_items,
-                           uint64_t items_per_block) {
+                           uint64_t items_per_block, int max_per_sm = 0) {
   int per_sm = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, smem) != cudaSuccess || per_sm < 1) per_sm = 1;
+  if (max_per_sm > 0 && per_sm > max_per_sm) per_sm = max_per_sm;
   uint64_t need = (work_items + items_per_block - 1) / items_per_block;
   if (need < 1) need = 1;
   const uint64_t fill = static_cast<uint64_t>(per_sm) * static_cast<uint64_t>(sm_count);

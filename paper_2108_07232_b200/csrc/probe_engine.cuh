@@ -80,6 +80,14 @@ __device__ __forceinline__ uint4 ldg_cg_v4(const void* p) {
   asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p) : "memory");
   return r;
 }
+// 16-byte load that ptxas may not narrow into the components actually consumed (two 4-byte loads would ask L2 for
+// every sector of the bucket twice): volatile = relaxed, system scope, served by L2 like .cg.
+__device__ __forceinline__ uint4 ldg_whole_v4(const void* p) {
+  uint4 r;
+  asm volatile("ld.volatile.global.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p) : "memory");
+  return r;
+}
+__device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
 __device__ __forceinline__ uint2 ldg_cg_v2(const void* p) {
   uint2 r;
   asm volatile("ld.global.cg.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p) : "memory");
@@ -153,6 +161,38 @@ __device__ __forceinline__ uint32_t staged_prefix_load(uint32_t base) {
   return q * S + prefix_below<S>(base, q * S);
 }
 
+// ---- direct load (insert side, register-resident) ------------------------------------------------
+// The bucket never touches shared memory: the C = B/2 lanes of a tile read one bucket with one 16-byte
+// LDG each (iteration u of a tile serves the key of the tile's u-th lane), count their empty slots and
+// add the counts up inside the tile (two ballots + popc).  load = B - empties (occupied slots form a prefix,
+// see staged_prefix_load).  No LDGSTS shared-memory write, no LDS: less work for the SM's load/store
+// pipe than the staged engine, at the price of B/2 x 4 registers held while the lines are in flight —
+// the trade that pays when the probes are L2-resident and few keys in flight suffice (routed builds).
+template <int B>
+__device__ __forceinline__ uint32_t direct_load(const uint64_t* __restrict__ store, uint32_t my_bid, int lane) {
+  static_assert(B >= 4 && B <= 16, "direct engine: 4 <= b <= 16");
+  constexpr int C = B / 2;
+  const int sub = lane & (C - 1);
+  const int tile_base = lane & ~(C - 1);
+  constexpr uint32_t kTileBits = (1u << C) - 1u;
+  uint4 v[C];
+#pragma unroll
+  for (int u = 0; u < C; ++u) {
+    const uint32_t bid = __shfl_sync(kFullMask, my_bid, tile_base + u);
+    v[u] = make_uint4(0u, 0u, 0u, 0u);
+    if (bid != kNoBucket) v[u] = ldg_whole_v4(store + static_cast<uint64_t>(bid) * B + sub * 2);
+  }
+  uint32_t empties = 0;
+#pragma unroll
+  for (int u = 0; u < C; ++u) {
+    const uint32_t e0 = __ballot_sync(kFullMask, v[u].x == kEmptyKey) >> tile_base;
+    const uint32_t e1 = __ballot_sync(kFullMask, v[u].z == kEmptyKey) >> tile_base;
+    const uint32_t s = __popc(e0 & kTileBits) + __popc(e1 & kTileBits);
+    if (sub == u) empties = s;
+  }
+  return B - empties;
+}
+
 // ---- scan -------------------------------------------------------------------------------------
 // The lane's own bucket: staged sizes read row `lane` of `stage`; b <= 2 loads straight from
 // global memory through L2.  WANT_KEY = false skips the key match (insert needs the load only).
@@ -217,6 +257,8 @@ struct TableView {
   uint32_t max_chain;
   uint32_t prose;
   uint32_t retry_cap;  // bound on CAS-loss retries per key (a legit table needs <= 3*b)
+  uint32_t chunk_log2;  // log2 of the work-stream chunk (see Stream)
+  uint32_t sweep_ahead_bytes;  // routed builds: how far ahead of the insert window the store is prefetched into L2
 };
 
 // h_i(key) with a per-lane i: the constants are picked with selects (a divergent constant-bank
@@ -259,38 +301,66 @@ __device__ __forceinline__ uint64_t pack_pair(uint32_t key, uint32_t value) {
 }
 
 // ---- work distribution ------------------------------------------------------------------------
-// The input is cut into chunks of kChunk elements that are dealt round-robin to the warps of the
-// grid, so at any moment the keys in flight form one narrow window that slides over the input (input
-// that is grouped by table region therefore probes one L2-sized region at a time).  Every warp streams
-// through its chunks as a lane-level state machine: a lane that has finished its key takes the next
-// unread key of the warp's stream, so every probe round is dense (32 probes per warp) no matter how
-// many rounds individual keys need.  The next 32 keys of the stream are prefetched one round ahead and
-// handed out with a shuffle.
-constexpr uint32_t kChunk = 256;
+// The input is cut into chunks of 2^chunk_log2 elements.  Chunk w goes to warp w of the grid; every further
+// chunk is claimed from a global cursor (one atomicAdd per chunk, issued one chunk ahead so its latency is
+// never waited for) by whichever warp runs dry first.  So the keys in flight always form one narrow window
+// that slides over the input in order — input that is grouped by table region therefore probes one L2-sized
+// region at a time — and no warp is left with a tail of work when the others are done.
+// Every warp streams through its chunks as a lane-level state machine: a lane that has finished its key
+// takes the next unread key of the warp's stream, so every probe round is dense (32 probes per warp) no
+// matter how many rounds individual keys need.  The next 32 keys of the stream are prefetched one round
+// ahead and handed out with a shuffle.
+constexpr uint32_t kDefaultChunkLog2 = 8;
 
 struct Stream {
-  uint32_t warp, n_warps;
-  uint32_t len, cursor;  // stream length and next unread position, in stream coordinates
+  uint32_t n_chunks, last_len;  // the last chunk may be partial
+  uint32_t cur, nxt;            // chunk held / chunk claimed ahead (warp-uniform); >= n_chunks = none
+  uint32_t cur_len;             // elements of `cur` (0 when none)
+  uint32_t pos;                 // next unread element of `cur`
 
-  // position in the warp's stream -> index into the caller's arrays
-  __device__ __forceinline__ uint64_t at(uint32_t p) const {
-    return (static_cast<uint64_t>(p / kChunk) * n_warps + warp) * kChunk + (p % kChunk);
+  __device__ __forceinline__ static uint32_t grid_warps() {
+    return static_cast<uint32_t>((static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5);
+  }
+  __device__ __forceinline__ uint32_t len_of(uint32_t chunk, uint32_t shift) const {
+    return chunk + 1 < n_chunks ? (1u << shift) : (chunk + 1 == n_chunks ? last_len : 0u);
+  }
+  // `cursor`: one global word per launch, zero at launch.  Nothing is claimed when the grid covers the input.
+  __device__ __forceinline__ uint32_t claim(uint32_t* cursor, int lane) const {
+    const uint32_t n_warps = grid_warps();
+    if (n_chunks <= n_warps) return n_chunks;
+    uint32_t c = 0;
+    if (lane == 0) c = atomicAdd(cursor, 1u);
+    return n_warps + __shfl_sync(kFullMask, c, 0);
+  }
+  __device__ __forceinline__ void init(uint64_t n, uint32_t shift, uint32_t* cursor, int lane) {
+    n_chunks = static_cast<uint32_t>((n + (1ull << shift) - 1) >> shift);
+    last_len = static_cast<uint32_t>(n - (static_cast<uint64_t>(n_chunks - (n != 0)) << shift));
+    cur = static_cast<uint32_t>((static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5);
+    cur_len = len_of(cur, shift);
+    pos = 0;
+    nxt = claim(cursor, lane);
+  }
+  // Global index of stream element pos + off (off < 32); false when the stream ends before it.
+  __device__ __forceinline__ bool index(uint32_t off, uint32_t shift, uint64_t& idx) const {
+    const uint32_t p = pos + off;
+    idx = (static_cast<uint64_t>(cur) << shift) + p;
+    if (pos + 32 <= cur_len) return true;  // warp-uniform: `nxt` (maybe still in flight) is not touched
+    if (p < cur_len) return true;
+    const uint32_t q = p - cur_len;  // spills into the chunk claimed ahead (chunks hold >= 32 elements)
+    idx = (static_cast<uint64_t>(nxt) << shift) + q;
+    return cur_len != 0 && q < len_of(nxt, shift);
+  }
+  // k (<= 32) elements were handed out.
+  __device__ __forceinline__ void advance(uint32_t k, uint32_t shift, uint32_t* cursor, int lane) {
+    pos += k;
+    if (pos >= cur_len && cur_len != 0) {
+      pos -= cur_len;
+      cur = nxt;
+      cur_len = len_of(cur, shift);
+      if (cur_len != 0) nxt = claim(cursor, lane);
+    }
   }
 };
-
-__device__ __forceinline__ Stream warp_stream(uint64_t n) {
-  Stream s;
-  s.warp = static_cast<uint32_t>((static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5);
-  s.n_warps = static_cast<uint32_t>((static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5);
-  const uint64_t chunks = (n + kChunk - 1) / kChunk;
-  const uint64_t mine = s.warp < chunks ? (chunks - s.warp + s.n_warps - 1) / s.n_warps : 0;
-  uint64_t len = mine * kChunk;
-  // the globally last chunk may be partial; it is the last chunk of whichever warp owns it
-  if (mine != 0 && ((mine - 1) * s.n_warps + s.warp) == chunks - 1) len -= chunks * kChunk - n;
-  s.len = static_cast<uint32_t>(len);
-  s.cursor = 0;
-  return s;
-}
 
 // Threads per block for a kernel that stages `rows_per_lane` buckets of B slots per lane: keeps the
 // staging area of a block at or below 32 KiB so that several blocks share an SM.

@@ -295,6 +295,11 @@ class HashTable:
     def set_iht_prose_fallback(self, enabled: bool) -> None:
         _check(self._lib.bht_set_iht_prose_fallback(self._h, int(bool(enabled))))
 
+    def set_blocked_insert(self, mode) -> None:
+        """L2-blocked routing of device-resident inserts: 0 / False = never, 1 / True = when the sizes make it
+        pay (default), 2 = always."""
+        _check(self._lib.bht_set_blocked_insert(self._h, int(mode)))
+
     # -- the hot path
     def insert(self, keys, values=None, n: Optional[int] = None, stream=None, want_result: bool = True,
                as_kind=None) -> Optional[BuildOutcome]:

@@ -149,6 +149,49 @@ def test_build_parity(bht, ora, kind, b, lf, t):
         assert np.array_equal(host(got), want2)
 
 
+@pytest.mark.parametrize("kind,b,lf,t", CASES)
+def test_build_parity_routed(bht, ora, monkeypatch, kind, b, lf, t):
+    """The L2-blocked build (pairs routed by the table region of their first bucket, packed-pair input of the insert
+    kernels): same stored multiset, admissible, same answers as a sequential oracle build of the same pairs."""
+    n = 150_001  # not a multiple of the router's group / tile sizes
+    keys = unique_keys(n, 300 + b, extra=n)
+    present, absent = keys[:n], keys[n:]
+    values = random_values(n, 11 * b)
+    monkeypatch.setenv("BHT_REGION_MB", "1")
+    for attempt in range(20):
+        cfg = bht.make_config(kind, n, lf, b, threshold=t, seed=bht.mix_seed(13, 0x100 + attempt))
+        table = bht.HashTable(cfg, 0)
+        table.set_blocked_insert(2)  # route whatever the sizes (auto mode only routes multi-million-key batches)
+        outcome = table.insert(dev(present), dev(values))
+        if outcome.success:
+            break
+        table.close()
+    else:
+        pytest.skip("configuration does not build")
+    assert outcome.inserted == n and outcome.failed == 0
+    assert table.inserted() == n and table.occupied_slots() == n
+    assert table.count_inadmissible() == 0
+    store = table.download_store()
+    assert np.array_equal(stored_pairs(store), packed(present, values))
+    otab = ora.table(to_oracle_cfg(cfg))
+    otab.upload_store(store)
+    assert otab.check_admissibility() == 0
+    queries = np.concatenate([present, absent])
+    want, hits, probes = otab.find_bulk(queries)
+    assert hits == n and np.array_equal(want[:n], values) and np.all(want[n:] == EMPTY)
+    got, stats = table.find(dev(queries), want_stats=True)
+    assert np.array_equal(host(got), want) and stats.probes == probes
+    # a second routed batch into the non-empty table (unaligned device slices: the router's element-load path)
+    if kind in ("bcht", "1cht") and lf <= 0.9:
+        extra = absent[1:2001]
+        ev = random_values(2000, 5)
+        o2 = table.insert(dev(np.concatenate([[0], extra]))[1:], dev(np.concatenate([[0], ev]))[1:])
+        if o2.success:
+            got2 = host(table.find(dev(extra)))
+            assert np.array_equal(got2, ev)
+            assert table.occupied_slots() == n + 2000 and table.count_inadmissible() == 0
+
+
 def test_build_default_values_and_host_memory(bht, ora):
     """values=None -> value_for_key (table.cpp:234); host arrays go through the staged PCIe path."""
     n = 300_000

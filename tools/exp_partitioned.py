@@ -15,6 +15,7 @@ v = torch.from_numpy(values.view(np.int32)).to(dev)
 a, b, r = cfg.hashes[0]
 h0 = bht.hash_keys(a, b, r, k).view(torch.int32).long()
 table = bht.HashTable(cfg, 0)
+table.set_blocked_insert(False)  # the input is grouped here, not by the library
 out = torch.empty(n, dtype=torch.int32, device=dev)
 
 def timed(fn, reps=3):
