@@ -20,7 +20,6 @@ import json
 import os
 import subprocess
 import sys
-import tempfile
 import threading
 import time
 
@@ -49,55 +48,68 @@ def make_workload(n: int, seed: int):
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled DURING the timed region (B200_PROFILING.md recipe)."""
+    """SM clock and clock-event (throttle) reasons sampled DURING the timed region, every ~2 ms from a host thread
+    through NVML (the timed region of the default run lasts tens of milliseconds, too short for `nvidia-smi -lms`);
+    falls back to one `nvidia-smi` query per sample when NVML cannot be loaded."""
 
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    Q = "clocks.sm,clocks.max.sm,clocks_event_reasons.active"
 
-    def __init__(self, gpu_index: int):
-        self.path = tempfile.mktemp(suffix=".csv")
-        self.gpu = gpu_index
-        self.proc = None
+    def __init__(self, gpu_index: int, uuid: str | None = None):
+        self.gpu, self.uuid = gpu_index, uuid
+        self.samples, self.reason_bits = [], 0
+        self.sm_max = None
+        self._stop = threading.Event()
+        self._thread = None
+        self._nvml = None
+        self._handle = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            try:
+                self._handle = pynvml.nvmlDeviceGetHandleByUUID(uuid) if uuid else pynvml.nvmlDeviceGetHandleByIndex(gpu_index)
+            except pynvml.NVMLError:
+                self._handle = pynvml.nvmlDeviceGetHandleByIndex(gpu_index)
+            self.sm_max = float(pynvml.nvmlDeviceGetMaxClockInfo(self._handle, pynvml.NVML_CLOCK_SM))
+            self._nvml = pynvml
+        except Exception:  # noqa: BLE001  (no NVML on this host: nvidia-smi below)
+            self._nvml = None
+
+    def _sample_once(self):
+        if self._nvml is not None:
+            nv = self._nvml
+            self.samples.append(float(nv.nvmlDeviceGetClockInfo(self._handle, nv.NVML_CLOCK_SM)))
+            self.reason_bits |= int(nv.nvmlDeviceGetCurrentClocksEventReasons(self._handle))
+            return
+        r = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits"],
+                           capture_output=True, text=True, timeout=10)
+        p = [x.strip() for x in r.stdout.strip().split(",")]
+        self.samples.append(float(p[0]))
+        self.sm_max = float(p[1])
+        self.reason_bits |= int(p[2], 16)
+
+    def _loop(self):
+        while not self._stop.is_set():
+            try:
+                self._sample_once()
+            except Exception:  # noqa: BLE001
+                pass
+            self._stop.wait(0.002)
 
     def start(self):
-        try:
-            self.f = open(self.path, "w")
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f,
-                                         stderr=subprocess.DEVNULL)
-        except OSError:
-            self.proc = None
+        self._thread = threading.Thread(target=self._loop, daemon=True)
+        self._thread.start()
 
     def stop(self):
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except subprocess.TimeoutExpired:
-            self.proc.kill()
-        self.f.close()
-        sm, smax, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in open(self.path):
-            p = [x.strip() for x in line.split(",")]
-            if len(p) < 9:
-                continue
-            try:
-                sm.append(float(p[1]))
-                smax = float(p[2])
-            except ValueError:
-                continue
-            for name, v in zip(names, p[5:9]):
-                if v.lower().startswith("active"):
-                    reasons.add(name)
-        os.unlink(self.path)
-        # idle samples (before / between launches) sit at low clocks: take the median of the upper half
-        sm.sort()
-        load = sm[len(sm) // 2:] if sm else []
-        return {"sm_mhz": float(np.median(load)) if load else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        self._stop.set()
+        if self._thread is not None:
+            self._thread.join(timeout=15)
+        # NVML clock-event reason bits (nvml.h): the ones that invalidate a run, plus the power cap (kept and noted)
+        bits = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown", 0x4: "sw_power_cap",
+                0x80: "hw_power_brake_slowdown"}
+        reasons = sorted(name for bit, name in bits.items() if self.reason_bits & bit)
+        sm = sorted(self.samples)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": self.sm_max, "reasons": reasons,
+                "samples": len(sm), "source": "nvml" if self._nvml is not None else "nvidia-smi"}
 
 
 # ---- the reference arm: the reference's own CPU implementation -------------------------------------------------
@@ -208,7 +220,11 @@ def run_cuda(args):
 
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
     stream = torch.cuda.current_stream()
-    sampler = ClockSampler(local)
+    try:
+        uuid = "GPU-" + str(torch.cuda.get_device_properties(local).uuid)
+    except Exception:  # noqa: BLE001
+        uuid = None
+    sampler = ClockSampler(local, uuid)
 
     if world == 1:
         if args.device_keys:

@@ -197,8 +197,10 @@ cudaError_t launch_insert_kind(bht_table* t, PairSource src, uint64_t n, int max
   a.sm_count = t->sm_count;
   a.max_ctas_per_sm = max_ctas_per_sm;
   {
-    const char* e = std::getenv("BHT_DIRECT");  // experiment knob: 1 = direct engine everywhere, 2 = routed builds only
-    const int mode = e ? std::atoi(e) : 0;
+    // experiment knob: 0 = staged engine everywhere, 1 = direct engine everywhere (default: measured faster for
+    // 4 <= b <= 16 in caller order and in routed builds), 2 = direct for routed builds only
+    const char* e = std::getenv("BHT_DIRECT");
+    const int mode = e ? std::atoi(e) : 1;
     a.direct = mode == 1 || (mode == 2 && src.values == nullptr);
   }
   a.stream = stream;
@@ -226,10 +228,16 @@ cudaError_t launch_insert_kind(bht_table* t, PairSource src, uint64_t n, int max
 // pass.  BHT_REGION_MB (environment) overrides the region size; 0 disables blocking.
 uint32_t blocked_regions(const bht_table* t, uint64_t n) {
   const char* env = std::getenv("BHT_REGION_MB");
-  const long region_mb = env ? std::atol(env) : 32L;
+  const long region_mb = env ? std::atol(env) : 48L;
   if (region_mb <= 0 || t->blocked_insert == 0 || n > 0x7FFFFFFFull) return 1;
   const uint64_t store_bytes = t->cfg.capacity * sizeof(uint64_t);
   const bool forced = t->blocked_insert == 2;  // bht_set_blocked_insert(table, 2): route whatever the sizes (tests)
+  // Only the cuckoo tables are routed by default.  Processing the pairs in H0 order correlates arrival time with
+  // the first candidate bucket; evictions make bcht / 1cht indifferent to that (same probe counts, same success),
+  // but the balanced placements of bp2ht / iht are order-sensitive: early regions spill into everybody's second
+  // choice and the last regions find both candidates full (bp2ht b=16 LF 0.8, 50 M keys: 9302 pairs dropped).
+  const bool cuckoo = t->cfg.kind == BHT_BCHT || t->cfg.kind == BHT_ONE_CHT;
+  if (!forced && !cuckoo) return 1;
   if (!forced && (n < (4ull << 20) || store_bytes < (192ull << 20))) return 1;
   uint64_t r = (store_bytes + (static_cast<uint64_t>(region_mb) << 20) - 1) / (static_cast<uint64_t>(region_mb) << 20);
   if (forced && r < 4) r = 4;

@@ -9,7 +9,7 @@ nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw,memory.total --fo
 nproc > $OUT/nproc.txt
 for w in $WHAT; do
   case $w in
-    tests) timeout 1500 python -m pytest tests -x -q -m gpu > $OUT/pytest_gpu.log 2>&1; echo "pytest exit $?" >> $OUT/pytest_gpu.log; tail -5 $OUT/pytest_gpu.log;;
+    tests) timeout 1500 python -m pytest tests --maxfail=8 -q -m gpu > $OUT/pytest_gpu.log 2>&1; echo "pytest exit $?" >> $OUT/pytest_gpu.log; tail -5 $OUT/pytest_gpu.log;;
     smoke) timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "smoke exit $?" >> $OUT/smoke.log; tail -3 $OUT/smoke.log;;
     bench) timeout 900 python bench.py --steps 10 --warmup 3 > $OUT/bench.json 2> $OUT/bench.err; echo "bench exit $?"; cat $OUT/bench.json; tail -5 $OUT/bench.err;;
     benchref) timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > $OUT/bench_ref.json 2> $OUT/bench_ref.err; cat $OUT/bench_ref.json;;
@@ -20,6 +20,8 @@ for w in $WHAT; do
           python bench.py --steps 1 --warmup 3 --no-cpu-baseline > $OUT/ncu_find.log 2>&1
       timeout 900 ncu --set full --clock-control none --import-source on -k regex:bulk_insert -s 3 -c 1 -f -o $OUT/prof_insert \
           python bench.py --steps 1 --warmup 3 --no-cpu-baseline > $OUT/ncu_insert.log 2>&1
+      timeout 900 ncu --set full --clock-control none --import-source on -k regex:route_ -s 9 -c 3 -f -o $OUT/prof_route \
+          python bench.py --steps 1 --warmup 3 --no-cpu-baseline > $OUT/ncu_route.log 2>&1
       ls -la $OUT;;
     *) echo "unknown step $w";;
   esac
