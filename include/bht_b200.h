@@ -179,9 +179,12 @@ bht_status bht_failed_keys(bht_table* table, uint32_t* host_out, uint64_t max_ke
 /* iht only: select the prose variant of iht_insert (table.cpp:167-169, `prose_fallback`). */
 bht_status bht_set_iht_prose_fallback(bht_table* table, int32_t enabled);
 
-/* Large device-resident inserts into a store much bigger than the L2 are routed by table region first
- * (an L2-blocked build; same result set, different concurrent order).  mode 0 = never (caller order),
- * 1 = when the sizes make it pay (default), 2 = always (small tables too; used by the parity tests). */
+/* Large device-resident inserts into a store much bigger than the L2 are blocked by table region first
+ * (same result set, different concurrent order).  Cuckoo kinds: the pairs are binned by the shared-memory-sized
+ * region of their first bucket and every region is built in shared memory; the pairs whose first bucket is
+ * full then go through the general kernel.  mode 0 = never (caller order), 1 = when the sizes make it pay
+ * (default), 2 = always the L2-routed build, 3 = always the shared-memory-blocked build (2 and 3 also on small
+ * tables; used by the parity tests). */
 bht_status bht_set_blocked_insert(bht_table* table, int32_t mode);
 
 /* ---- load factor / store access ---------------------------------------------------------- */

@@ -86,7 +86,10 @@ struct bht_table {
   DevCounters* ctr = nullptr;       // device
   DevCounters* ctr_host = nullptr;  // pinned mirror
   uint32_t* failed_keys = nullptr;  // device log of dropped keys
-  int blocked_insert = 1;  // 0 = caller order, 1 = routed when worth it, 2 = always routed (bht_set_blocked_insert)
+  // bht_set_blocked_insert: 0 = caller order, 1 = blocked when worth it (default), 2 = always the L2-routed
+  // build, 3 = always the shared-memory-blocked build (cuckoo kinds; other kinds fall back to 2)
+  int blocked_insert = 1;
+  bool known_empty = true;  // no slot has been written since create / clear: a blocked build need not read the store
   uint32_t* cursors = nullptr;        // device: ring of per-launch work cursors (Stream, probe_engine.cuh)
   std::atomic<uint32_t> cursor_seq{0};
   Staging stage;
@@ -187,10 +190,13 @@ cudaError_t next_cursor(bht_table* t, cudaStream_t stream, uint32_t** out) {
   return cudaMemsetAsync(*out, 0, sizeof(uint32_t), stream);
 }
 
-cudaError_t launch_insert_kind(bht_table* t, PairSource src, uint64_t n, int max_ctas_per_sm, cudaStream_t stream) {
+cudaError_t launch_insert_kind(bht_table* t, PairSource src, uint64_t n, int max_ctas_per_sm, cudaStream_t stream,
+                               bool routed = false, const unsigned long long* n_dev = nullptr) {
   InsertLaunch a;
   a.src = src;
   a.n = n;
+  a.routed = routed;
+  a.n_dev = n_dev;
   a.ctr = t->ctr;
   a.failed_keys = t->failed_keys;
   a.failed_cap = kFailedLogCap;
@@ -201,7 +207,7 @@ cudaError_t launch_insert_kind(bht_table* t, PairSource src, uint64_t n, int max
     // 4 <= b <= 16 in caller order and in routed builds), 2 = direct for routed builds only
     const char* e = std::getenv("BHT_DIRECT");
     const int mode = e ? std::atoi(e) : 1;
-    a.direct = mode == 1 || (mode == 2 && src.values == nullptr);
+    a.direct = mode == 1 || (mode == 2 && routed);
   }
   a.stream = stream;
   cudaError_t e = next_cursor(t, stream, &a.work_cursor);
@@ -231,7 +237,7 @@ uint32_t blocked_regions(const bht_table* t, uint64_t n) {
   const long region_mb = env ? std::atol(env) : 48L;
   if (region_mb <= 0 || t->blocked_insert == 0 || n > 0x7FFFFFFFull) return 1;
   const uint64_t store_bytes = t->cfg.capacity * sizeof(uint64_t);
-  const bool forced = t->blocked_insert == 2;  // bht_set_blocked_insert(table, 2): route whatever the sizes (tests)
+  const bool forced = t->blocked_insert >= 2;  // bht_set_blocked_insert(table, 2): route whatever the sizes (tests)
   // Only the cuckoo tables are routed by default.  Processing the pairs in H0 order correlates arrival time with
   // the first candidate bucket; evictions make bcht / 1cht indifferent to that (same probe counts, same success),
   // but the balanced placements of bp2ht / iht are order-sensitive: early regions spill into everybody's second
@@ -244,6 +250,22 @@ uint32_t blocked_regions(const bht_table* t, uint64_t n) {
   if (r > static_cast<uint64_t>(kMaxShards)) r = kMaxShards;
   if (r >= t->cfg.num_buckets) r = t->cfg.num_buckets - 1;  // the router needs n_regions < hash range
   return static_cast<uint32_t>(r < 2 ? 1 : r);
+}
+
+// Plan of a shared-memory-blocked build (build_blocked.cu) of n device-resident pairs, n_regions == 0 when it is
+// not used.  It is opt-in — bht_set_blocked_insert(table, 3), or BHT_SMEM_BUILD=1 in the environment for the sizes
+// the L2-routed build would take — because today it only ties with the L2-routed build (see build_blocked.cu).
+BlockedPlan smem_blocked_plan(const bht_table* t, uint64_t n) {
+  BlockedPlan none{};
+  if (t->cfg.kind != BHT_BCHT || n == 0) return none;
+  const bool forced = t->blocked_insert == 3;
+  if (!forced) {
+    const char* env = std::getenv("BHT_SMEM_BUILD");
+    if (env == nullptr || std::atoi(env) == 0 || t->blocked_insert != 1) return none;
+    const uint64_t store_bytes = t->cfg.capacity * sizeof(uint64_t);
+    if (n < (4ull << 20) || store_bytes < (192ull << 20) || n * 8 < t->cfg.capacity) return none;
+  }
+  return plan_blocked_build(t->view, n);
 }
 
 // Resident CTAs per SM of the insert kernel of a routed build: with the probes L2-resident a few hundred keys in
@@ -272,8 +294,23 @@ bht_status do_insert(bht_table* t, const uint32_t* keys, const uint32_t* values,
 
   BHT_CUDA(cudaMemsetAsync(t->ctr, 0, kPerCallCounterBytes, stream));
   if (mem_space == BHT_MEM_DEVICE) {
-    const uint32_t regions = blocked_regions(t, n);
-    if (regions > 1) {
+    const BlockedPlan plan = smem_blocked_plan(t, n);
+    const uint32_t regions = plan.n_regions != 0 ? 1 : blocked_regions(t, n);
+    if (plan.n_regions != 0) {
+      // Shared-memory-blocked build (build_blocked.cu): bin the pairs by the shared-memory-sized table region of
+      // their first bucket, build every region in shared memory, then run the general kernel over the pairs whose
+      // first bucket was full (their count stays on the device).
+      void* scratch = nullptr;
+      BHT_CUDA(cudaMallocAsync(&scratch, blocked_scratch_bytes(plan, n), stream));
+      const uint2* spill = nullptr;
+      const unsigned long long* spill_count = nullptr;
+      cudaError_t e = launch_blocked_build(t->view, plan, keys, values, n, t->known_empty, scratch, t->ctr, t->sm_count, stream,
+                                           &spill, &spill_count);
+      if (e == cudaSuccess)
+        e = launch_insert_kind(t, PairSource{reinterpret_cast<const uint32_t*>(spill), nullptr}, n, 0, stream, false, spill_count);
+      cudaFreeAsync(scratch, stream);
+      if (e != cudaSuccess) return cuda_fail(e, "bht_insert (shared-memory blocked)");
+    } else if (regions > 1) {
       // L2-blocked build: group the pairs by the table region of their first bucket, then insert region by
       // region, so that bucket fetches, claims and the write-back of dirty sectors happen while the region
       // is L2-resident (the probe kernels deal their input out as one sliding window, probe_engine.cuh).
@@ -283,7 +320,7 @@ bht_status do_insert(bht_table* t, const uint32_t* keys, const uint32_t* values,
       uint8_t* dest8 = reinterpret_cast<uint8_t*>(counts + 2 * regions);
       cudaError_t e = launch_region_route(t->view.h[0], regions, keys, values, n, dest8, counts, counts + regions, scratch,
                                           t->sm_count, stream);
-      if (e == cudaSuccess) e = launch_insert_kind(t, PairSource{scratch, nullptr}, n, blocked_ctas_per_sm(), stream);
+      if (e == cudaSuccess) e = launch_insert_kind(t, PairSource{scratch, nullptr}, n, blocked_ctas_per_sm(), stream, true);
       cudaFreeAsync(scratch, stream);
       if (e != cudaSuccess) return cuda_fail(e, "bht_insert (blocked)");
     } else {
@@ -312,6 +349,7 @@ bht_status do_insert(bht_table* t, const uint32_t* keys, const uint32_t* values,
     BHT_CUDA(cudaStreamWaitEvent(stream, st.kernel_done[(chunks - 1) % kStageSlots], 0));
     BHT_CUDA(cudaStreamSynchronize(stream));  // the caller's host arrays are free again on return
   }
+  if (n != 0) t->known_empty = false;
   if (result != nullptr) {
     bht_status s = read_counters(t, stream);
     if (s != BHT_OK) return s;
@@ -560,6 +598,7 @@ bht_status bht_clear(bht_table* t, void* stream) {
   std::lock_guard<std::mutex> lock(t->mu);
   BHT_CUDA(launch_fill_empty(t->view.store, t->cfg.capacity, t->sm_count, as_stream(stream)));
   BHT_CUDA(cudaMemsetAsync(t->ctr, 0, sizeof(DevCounters), as_stream(stream)));
+  t->known_empty = true;
   return BHT_OK;
 }
 
@@ -656,7 +695,7 @@ bht_status bht_set_iht_prose_fallback(bht_table* t, int32_t enabled) {
 
 bht_status bht_set_blocked_insert(bht_table* t, int32_t enabled) {
   if (t == nullptr) return fail(BHT_INVALID_ARGUMENT, "bht_set_blocked_insert: null table");
-  if (enabled < 0 || enabled > 2) return fail(BHT_INVALID_ARGUMENT, "bht_set_blocked_insert: mode must be 0, 1 or 2");
+  if (enabled < 0 || enabled > 3) return fail(BHT_INVALID_ARGUMENT, "bht_set_blocked_insert: mode must be 0, 1, 2 or 3");
   t->blocked_insert = enabled;
   return BHT_OK;
 }
@@ -714,6 +753,7 @@ bht_status bht_upload_store(bht_table* t, const uint64_t* host_src, void* stream
   BHT_ON_DEVICE(t->device);
   std::lock_guard<std::mutex> lock(t->mu);
   cudaStream_t s = as_stream(stream);
+  t->known_empty = false;
   BHT_CUDA(cudaMemcpyAsync(t->view.store, host_src, t->cfg.capacity * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
   BHT_CUDA(cudaMemsetAsync(t->ctr, 0, sizeof(DevCounters), s));
   BHT_CUDA(launch_count_occupied(t->view.store, t->cfg.capacity, &t->ctr->inserted_total, t->sm_count, s));
@@ -743,7 +783,11 @@ bht_status bht_dump_store(const bht_table* t, const char* path) {
   return BHT_OK;
 }
 
-uint64_t* bht_device_store(const bht_table* t) { return t ? t->view.store : nullptr; }
+uint64_t* bht_device_store(const bht_table* t) {
+  if (t == nullptr) return nullptr;
+  const_cast<bht_table*>(t)->known_empty = false;  // the caller may write slots behind the library's back
+  return t->view.store;
+}
 
 // ---- hash stage in isolation ----------------------------------------------------------------------
 

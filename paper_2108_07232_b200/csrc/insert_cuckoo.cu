@@ -27,11 +27,13 @@ namespace bht_b200 {
 template <int B, int H, bool DIRECT>
 __global__ void __launch_bounds__(block_threads<B>(1), DIRECT ? 3 : 6)
 bulk_insert_cuckoo_kernel(const __grid_constant__ TableView t, const PairSource src, uint64_t n,
+                          const unsigned long long* __restrict__ n_dev, const bool routed,
                           DevCounters* __restrict__ ctr, uint32_t* __restrict__ failed_keys, uint64_t failed_cap,
                           uint32_t* __restrict__ work_cursor) {
   using G = Geo<B>;
   extern __shared__ __align__(1024) unsigned char smem[];
   const int lane = threadIdx.x & 31;
+  if (n_dev != nullptr) n = min(n, static_cast<uint64_t>(*n_dev));  // spill list of a blocked build: counted on the device
   const uint32_t stage = DIRECT ? 0u : smem_u32(smem) + (threadIdx.x >> 5) * G::WARP_BYTES;
   unsigned long long* store = reinterpret_cast<unsigned long long*>(t.store);
 
@@ -55,7 +57,6 @@ bulk_insert_cuckoo_kernel(const __grid_constant__ TableView t, const PairSource 
   // touches of a bucket are L2 hits.  (2) A bucket outside the region (the next bucket of an evicted pair) is
   // prefetched as soon as it is known and the lane sits one round out; it reads the line when it has arrived.
   // Every round of a warp then waits for L2, not for the slowest HBM access among its 32 lanes.
-  const bool routed = src.values == nullptr;  // kernel-uniform
   const uint32_t lines_per_bucket = (B * 8 + 127) / 128;
   const uint64_t n_lines = (t.num_buckets * B * 8 + 127) / 128;
   uint32_t swept_chunk = 0xFFFFFFFFu;
@@ -164,7 +165,7 @@ static cudaError_t launch_one(const TableView& t, const InsertLaunch& a) {
       auto kernel = bulk_insert_cuckoo_kernel<B, H, true>;
       constexpr int block = block_threads<B>(1);
       const int grid = persistent_grid(kernel, block, 0, a.sm_count, a.n, block, a.max_ctas_per_sm);
-      kernel<<<grid, block, 0, a.stream>>>(t, a.src, a.n, a.ctr, a.failed_keys, a.failed_cap, a.work_cursor);
+      kernel<<<grid, block, 0, a.stream>>>(t, a.src, a.n, a.n_dev, a.routed, a.ctr, a.failed_keys, a.failed_cap, a.work_cursor);
       note_launch();
       return cudaGetLastError();
     }
@@ -173,7 +174,7 @@ static cudaError_t launch_one(const TableView& t, const InsertLaunch& a) {
   constexpr int block = block_threads<B>(1);
   constexpr int smem = (block / 32) * Geo<B>::WARP_BYTES;
   const int grid = persistent_grid(kernel, block, smem, a.sm_count, a.n, block, a.max_ctas_per_sm);
-  kernel<<<grid, block, smem, a.stream>>>(t, a.src, a.n, a.ctr, a.failed_keys, a.failed_cap, a.work_cursor);
+  kernel<<<grid, block, smem, a.stream>>>(t, a.src, a.n, a.n_dev, a.routed, a.ctr, a.failed_keys, a.failed_cap, a.work_cursor);
   note_launch();
   return cudaGetLastError();
 }

@@ -30,6 +30,8 @@ struct InsertLaunch {
   int sm_count;
   int max_ctas_per_sm;    // 0 = whatever fits; a routed (L2-blocked) build keeps fewer keys in flight
   bool direct;            // cuckoo, 4 <= b <= 16: register-resident probe (direct_load) instead of the staged one
+  bool routed = false;    // cuckoo: the pairs arrive grouped by table region in table order (L2-blocked build)
+  const unsigned long long* n_dev = nullptr;  // cuckoo: when set, the pair count is read on the device (<= n)
   cudaStream_t stream;
 };
 
@@ -37,6 +39,23 @@ struct InsertLaunch {
 cudaError_t launch_insert_cuckoo(const TableView& t, const InsertLaunch& a);
 cudaError_t launch_insert_p2(const TableView& t, const InsertLaunch& a);
 cudaError_t launch_insert_iht(const TableView& t, const InsertLaunch& a);
+
+// build_blocked.cu — K10 bin_scatter + K11 region_build: the shared-memory-blocked first pass of a cuckoo build.
+constexpr uint32_t kMaxBlockedRegions = 40000;  // 16-bit region ids, histogram of one tile in shared memory
+struct BlockedPlan {
+  uint32_t n_regions;    // 0: the blocked build does not apply
+  uint32_t region_log2;  // buckets per region (64 KiB of slots)
+  uint32_t b_log2;
+  uint32_t cap;          // pairs per bin
+  uint32_t cursor_shift; // bin cursors are 4 << cursor_shift bytes apart
+};
+BlockedPlan plan_blocked_build(const TableView& t, uint64_t n);
+size_t blocked_scratch_bytes(const BlockedPlan& p, uint64_t n);
+// Places every pair whose H0 bucket has room; the others are left in *spill_out (packed pairs, *spill_count_out of
+// them, both device pointers into `scratch`) for launch_insert_cuckoo.
+cudaError_t launch_blocked_build(const TableView& t, const BlockedPlan& p, const uint32_t* keys, const uint32_t* values,
+                                 uint64_t n, bool fresh, void* scratch, DevCounters* ctr, int sm_count, cudaStream_t stream,
+                                 const uint2** spill_out, const unsigned long long** spill_count_out);
 
 // util.cu — K0 fill, K7 count, admissibility, hash hook, K8/K9 shard routing, synthetic keys.
 cudaError_t launch_fill_empty(uint64_t* store, uint64_t n_slots, int sm_count, cudaStream_t stream);

@@ -296,8 +296,8 @@ class HashTable:
         _check(self._lib.bht_set_iht_prose_fallback(self._h, int(bool(enabled))))
 
     def set_blocked_insert(self, mode) -> None:
-        """L2-blocked routing of device-resident inserts: 0 / False = never, 1 / True = when the sizes make it
-        pay (default), 2 = always."""
+        """Blocked builds of device-resident inserts: 0 / False = never (caller order), 1 / True = when the sizes
+        make it pay (default), 2 = always the L2-routed build, 3 = always the shared-memory-blocked build."""
         _check(self._lib.bht_set_blocked_insert(self._h, int(mode)))
 
     # -- the hot path

@@ -149,10 +149,13 @@ def test_build_parity(bht, ora, kind, b, lf, t):
         assert np.array_equal(host(got), want2)
 
 
+@pytest.mark.parametrize("mode", [2, 3])
 @pytest.mark.parametrize("kind,b,lf,t", CASES)
-def test_build_parity_routed(bht, ora, monkeypatch, kind, b, lf, t):
-    """The L2-blocked build (pairs routed by the table region of their first bucket, packed-pair input of the insert
-    kernels): same stored multiset, admissible, same answers as a sequential oracle build of the same pairs."""
+def test_build_parity_routed(bht, ora, monkeypatch, kind, b, lf, t, mode):
+    """The blocked builds — mode 2: pairs routed by the L2-sized table region of their first bucket (packed-pair input
+    of the insert kernels); mode 3: pairs binned by shared-memory-sized region, regions built in shared memory, the
+    rest through the general kernel — give the same stored multiset, admissible, same answers as a sequential oracle
+    build of the same pairs."""
     n = 150_001  # not a multiple of the router's group / tile sizes
     keys = unique_keys(n, 300 + b, extra=n)
     present, absent = keys[:n], keys[n:]
@@ -161,7 +164,7 @@ def test_build_parity_routed(bht, ora, monkeypatch, kind, b, lf, t):
     for attempt in range(20):
         cfg = bht.make_config(kind, n, lf, b, threshold=t, seed=bht.mix_seed(13, 0x100 + attempt))
         table = bht.HashTable(cfg, 0)
-        table.set_blocked_insert(2)  # route whatever the sizes (auto mode only routes multi-million-key batches)
+        table.set_blocked_insert(mode)  # whatever the sizes (auto mode only blocks multi-million-key batches)
         outcome = table.insert(dev(present), dev(values))
         if outcome.success:
             break
