@@ -176,6 +176,11 @@ bht_status bht_find_exhaustive(const bht_table* table, const uint32_t* keys, uin
 bht_status bht_last_insert_result(bht_table* table, bht_insert_result* out, void* stream);
 /* Keys dropped by inserts since the last bht_clear (at most `max_keys` copied). */
 bht_status bht_failed_keys(bht_table* table, uint32_t* host_out, uint64_t max_keys, uint64_t* count);
+/* Device time of the last device-resident bht_insert, split at the launch of its probe kernel: `prepare_ms` =
+ * routing / binning passes of a blocked build (0 in caller order), `probe_ms` = the bulk-insert kernel itself.
+ * Measured with CUDA events on the call's stream; waits for that call to finish.  (Instrumentation for the
+ * per-kernel roofline; the reference's counterpart is the steady_clock around build(), table.cpp:228-276.) */
+bht_status bht_last_insert_phases(bht_table* table, float* prepare_ms, float* probe_ms);
 /* iht only: select the prose variant of iht_insert (table.cpp:167-169, `prose_fallback`). */
 bht_status bht_set_iht_prose_fallback(bht_table* table, int32_t enabled);
 

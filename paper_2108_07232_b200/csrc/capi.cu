@@ -63,6 +63,16 @@ struct DeviceScope {  // every call runs on the table's device and leaves the ca
 
 constexpr int kStageSlots = 3;
 constexpr uint64_t kStageChunk = 1ull << 22;  // keys per staged chunk: 16 MiB per array over PCIe
+constexpr uint64_t kStageChunkMin = 1ull << 18;
+
+// Length of the staged chunk that starts at `off`: chunks double from kStageChunkMin up to kStageChunk and halve
+// again towards the end, so the pipeline fills and drains in ~1 MiB steps (the first copy-in and the last
+// kernel / copy-out are the only parts of a host-buffer call that nothing overlaps).
+uint64_t stage_chunk_len(uint64_t off, uint64_t n) {
+  const uint64_t up = std::max(kStageChunkMin, off);
+  const uint64_t down = std::max(kStageChunkMin, (n - off) / 2);
+  return std::min(std::min(kStageChunk, n - off), std::min(up, down));
+}
 constexpr uint64_t kFailedLogCap = 1ull << 20;
 constexpr uint32_t kRetryCap = 1024;
 
@@ -90,6 +100,10 @@ struct bht_table {
   // build, 3 = always the shared-memory-blocked build (cuckoo kinds; other kinds fall back to 2)
   int blocked_insert = 1;
   bool known_empty = true;  // no slot has been written since create / clear: a blocked build need not read the store
+  // device-resident bht_insert: events around the preparation (routing / binning) and the probe kernel of the last
+  // call, for bht_last_insert_phases (per-kernel roofline of bench.py)
+  cudaEvent_t phase_ev[3] = {};
+  bool phases_recorded = false;
   uint32_t* cursors = nullptr;        // device: ring of per-launch work cursors (Stream, probe_engine.cuh)
   std::atomic<uint32_t> cursor_seq{0};
   Staging stage;
@@ -294,6 +308,7 @@ bht_status do_insert(bht_table* t, const uint32_t* keys, const uint32_t* values,
 
   BHT_CUDA(cudaMemsetAsync(t->ctr, 0, kPerCallCounterBytes, stream));
   if (mem_space == BHT_MEM_DEVICE) {
+    BHT_CUDA(cudaEventRecord(t->phase_ev[0], stream));
     const BlockedPlan plan = smem_blocked_plan(t, n);
     const uint32_t regions = plan.n_regions != 0 ? 1 : blocked_regions(t, n);
     if (plan.n_regions != 0) {
@@ -306,6 +321,7 @@ bht_status do_insert(bht_table* t, const uint32_t* keys, const uint32_t* values,
       const unsigned long long* spill_count = nullptr;
       cudaError_t e = launch_blocked_build(t->view, plan, keys, values, n, t->known_empty, scratch, t->ctr, t->sm_count, stream,
                                            &spill, &spill_count);
+      if (e == cudaSuccess) e = cudaEventRecord(t->phase_ev[1], stream);
       if (e == cudaSuccess)
         e = launch_insert_kind(t, PairSource{reinterpret_cast<const uint32_t*>(spill), nullptr}, n, 0, stream, false, spill_count);
       cudaFreeAsync(scratch, stream);
@@ -320,12 +336,16 @@ bht_status do_insert(bht_table* t, const uint32_t* keys, const uint32_t* values,
       uint8_t* dest8 = reinterpret_cast<uint8_t*>(counts + 2 * regions);
       cudaError_t e = launch_region_route(t->view.h[0], regions, keys, values, n, dest8, counts, counts + regions, scratch,
                                           t->sm_count, stream);
+      if (e == cudaSuccess) e = cudaEventRecord(t->phase_ev[1], stream);
       if (e == cudaSuccess) e = launch_insert_kind(t, PairSource{scratch, nullptr}, n, blocked_ctas_per_sm(), stream, true);
       cudaFreeAsync(scratch, stream);
       if (e != cudaSuccess) return cuda_fail(e, "bht_insert (blocked)");
     } else {
+      BHT_CUDA(cudaEventRecord(t->phase_ev[1], stream));
       BHT_CUDA(launch_insert_kind(t, PairSource{keys, values}, n, 0, stream));
     }
+    BHT_CUDA(cudaEventRecord(t->phase_ev[2], stream));
+    t->phases_recorded = true;
   } else if (n != 0) {
     bht_status s = ensure_staging(t);
     if (s != BHT_OK) return s;
@@ -333,11 +353,11 @@ bht_status do_insert(bht_table* t, const uint32_t* keys, const uint32_t* values,
     cudaEvent_t start = st.out_done[0];  // reuse as the "counters are zeroed" marker
     BHT_CUDA(cudaEventRecord(start, stream));
     BHT_CUDA(cudaStreamWaitEvent(st.compute, start, 0));
-    const uint64_t chunks = (n + kStageChunk - 1) / kStageChunk;
-    for (uint64_t c = 0; c < chunks; ++c) {
+    uint64_t chunks = 0;
+    for (uint64_t c = 0, off = 0; off < n; ++c) {
       const int slot = static_cast<int>(c % kStageSlots);
-      const uint64_t off = c * kStageChunk;
-      const uint64_t len = std::min(kStageChunk, n - off);
+      const uint64_t len = stage_chunk_len(off, n);
+      chunks = c + 1;
       if (c >= kStageSlots) BHT_CUDA(cudaStreamWaitEvent(st.h2d, st.kernel_done[slot], 0));
       BHT_CUDA(cudaMemcpyAsync(st.keys[slot], keys + off, len * sizeof(uint32_t), cudaMemcpyHostToDevice, st.h2d));
       BHT_CUDA(cudaMemcpyAsync(st.vals[slot], values + off, len * sizeof(uint32_t), cudaMemcpyHostToDevice, st.h2d));
@@ -345,6 +365,7 @@ bht_status do_insert(bht_table* t, const uint32_t* keys, const uint32_t* values,
       BHT_CUDA(cudaStreamWaitEvent(st.compute, st.in_done[slot], 0));
       BHT_CUDA(launch_insert_kind(t, PairSource{st.keys[slot], st.vals[slot]}, len, 0, st.compute));
       BHT_CUDA(cudaEventRecord(st.kernel_done[slot], st.compute));
+      off += len;
     }
     BHT_CUDA(cudaStreamWaitEvent(stream, st.kernel_done[(chunks - 1) % kStageSlots], 0));
     BHT_CUDA(cudaStreamSynchronize(stream));  // the caller's host arrays are free again on return
@@ -390,11 +411,11 @@ bht_status do_find(const bht_table* ct, bool early_exit, const uint32_t* keys, u
     cudaEvent_t start = st.in_done[0];
     BHT_CUDA(cudaEventRecord(start, stream));
     BHT_CUDA(cudaStreamWaitEvent(st.compute, start, 0));
-    const uint64_t chunks = (n + kStageChunk - 1) / kStageChunk;
-    for (uint64_t c = 0; c < chunks; ++c) {
+    uint64_t chunks = 0;
+    for (uint64_t c = 0, off = 0; off < n; ++c) {
       const int slot = static_cast<int>(c % kStageSlots);
-      const uint64_t off = c * kStageChunk;
-      const uint64_t len = std::min(kStageChunk, n - off);
+      const uint64_t len = stage_chunk_len(off, n);
+      chunks = c + 1;
       if (c >= kStageSlots) {
         BHT_CUDA(cudaStreamWaitEvent(st.h2d, st.kernel_done[slot], 0));   // keys[slot] consumed
         BHT_CUDA(cudaStreamWaitEvent(st.compute, st.out_done[slot], 0));  // vals[slot] drained
@@ -409,6 +430,7 @@ bht_status do_find(const bht_table* ct, bool early_exit, const uint32_t* keys, u
       BHT_CUDA(cudaStreamWaitEvent(st.d2h, st.kernel_done[slot], 0));
       BHT_CUDA(cudaMemcpyAsync(out + off, st.vals[slot], len * sizeof(uint32_t), cudaMemcpyDeviceToHost, st.d2h));
       BHT_CUDA(cudaEventRecord(st.out_done[slot], st.d2h));
+      off += len;
     }
     BHT_CUDA(cudaStreamWaitEvent(stream, st.kernel_done[(chunks - 1) % kStageSlots], 0));
     BHT_CUDA(cudaStreamSynchronize(st.d2h));  // answers are in the caller's host array on return
@@ -544,6 +566,7 @@ bht_status bht_create(const bht_config* cfg, int32_t device, bht_table** out) {
   if (e == cudaSuccess) e = cudaMallocHost(&t->ctr_host, sizeof(DevCounters));
   if (e == cudaSuccess) e = cudaMalloc(&t->failed_keys, kFailedLogCap * sizeof(uint32_t));
   if (e == cudaSuccess) e = cudaMalloc(&t->cursors, kCursorSlots * sizeof(uint32_t));
+  for (int i = 0; i < 3 && e == cudaSuccess; ++i) e = cudaEventCreate(&t->phase_ev[i]);
   if (e == cudaSuccess) e = cudaMemset(t->ctr, 0, sizeof(DevCounters));
   if (e == cudaSuccess) e = launch_fill_empty(store, cfg->capacity, t->sm_count, nullptr);
   if (e == cudaSuccess) e = cudaStreamSynchronize(nullptr);
@@ -588,6 +611,8 @@ bht_status bht_destroy(bht_table* t) {
   cudaFreeHost(t->ctr_host);
   cudaFree(t->failed_keys);
   cudaFree(t->cursors);
+  for (cudaEvent_t ev : t->phase_ev)
+    if (ev) cudaEventDestroy(ev);
   delete t;
   return BHT_OK;
 }
@@ -683,6 +708,18 @@ bht_status bht_failed_keys(bht_table* t, uint32_t* host_out, uint64_t max_keys, 
   const uint64_t n = std::min<uint64_t>(std::min<uint64_t>(*count, kFailedLogCap), max_keys);
   if (n != 0 && host_out != nullptr)
     BHT_CUDA(cudaMemcpy(host_out, t->failed_keys, n * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+  return BHT_OK;
+}
+
+bht_status bht_last_insert_phases(bht_table* t, float* prepare_ms, float* probe_ms) {
+  if (t == nullptr || prepare_ms == nullptr || probe_ms == nullptr)
+    return fail(BHT_INVALID_ARGUMENT, "bht_last_insert_phases: null argument");
+  BHT_ON_DEVICE(t->device);
+  std::lock_guard<std::mutex> lock(t->mu);
+  if (!t->phases_recorded) return fail(BHT_INVALID_ARGUMENT, "bht_last_insert_phases: no device-resident insert yet");
+  BHT_CUDA(cudaEventSynchronize(t->phase_ev[2]));
+  BHT_CUDA(cudaEventElapsedTime(prepare_ms, t->phase_ev[0], t->phase_ev[1]));
+  BHT_CUDA(cudaEventElapsedTime(probe_ms, t->phase_ev[1], t->phase_ev[2]));
   return BHT_OK;
 }
 

@@ -335,6 +335,13 @@ class HashTable:
         return BuildOutcome(bool(res.success), res.inserted, res.failed, res.attempted, res.probes,
                             None if res.first_failed_key == EMPTY_KEY else res.first_failed_key)
 
+    def last_insert_phases(self):
+        """(prepare_ms, probe_ms) of the last device-resident insert: routing / binning passes, then the bulk-insert
+        kernel, timed with CUDA events inside the library."""
+        a, b = C.c_float(), C.c_float()
+        _check(self._lib.bht_last_insert_phases(self._h, C.byref(a), C.byref(b)))
+        return float(a.value), float(b.value)
+
     def failed_keys(self, max_keys: int = 1 << 20) -> np.ndarray:
         buf = np.empty(max_keys, dtype=np.uint32)
         cnt = C.c_uint64()
