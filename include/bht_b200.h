@@ -189,7 +189,8 @@ bht_status bht_set_iht_prose_fallback(bht_table* table, int32_t enabled);
  * region of their first bucket and every region is built in shared memory; the pairs whose first bucket is
  * full then go through the general kernel.  mode 0 = never (caller order), 1 = when the sizes make it pay
  * (default), 2 = always the L2-routed build, 3 = always the shared-memory-blocked build (2 and 3 also on small
- * tables; used by the parity tests). */
+ * tables; used by the parity tests).  bp2ht / iht are never blocked: their balanced placements depend on the
+ * arrival order, and arrival in first-bucket order measurably lowers the load factor they reach. */
 bht_status bht_set_blocked_insert(bht_table* table, int32_t mode);
 
 /* ---- load factor / store access ---------------------------------------------------------- */
@@ -240,6 +241,27 @@ bht_status bht_shard_unpermute(const uint32_t* answers, const uint32_t* index, u
  * host-side rejection set.  Indices >= some n are guaranteed-absent negatives. */
 bht_status bht_generate_unique_keys(uint64_t seed, uint64_t offset, uint64_t n, uint32_t* out_keys,
                                     uint32_t* out_values, int32_t device, void* stream);
+
+/* generate_keys (keygen.cpp:50-64), element for element: the first n distinct non-sentinel values of
+ * (std::mt19937_64(seed)() >> 32) in stream order.  The engine runs on the host in batches; "first occurrence
+ * wins" is decided by a device hash set (atomicMin on the stream index) and an order-preserving compaction.
+ * out_keys: n words in `mem_space`. */
+bht_status bht_generate_keys(uint64_t seed, uint64_t n, uint32_t* out_keys, int32_t mem_space, int32_t device,
+                             void* stream);
+
+/* generate_queries (keygen.cpp:66-98), element for element: round(positive_ratio * q) positives by a partial
+ * Fisher-Yates over the key list, the rest guaranteed-absent draws of the same stream (membership = a bulk find
+ * on a device table of the keys), then shuffle_deterministic.  keys: n_keys words in `keys_space`; the three
+ * outputs are HOST arrays of q elements (out_expected = value_for_key for positives, 0 for negatives;
+ * out_expected / out_present may be null).  BHT_INVALID_ARGUMENT where the reference throws invalid_argument. */
+bht_status bht_generate_queries(const uint32_t* keys, uint64_t n_keys, int32_t keys_space, double positive_ratio,
+                                uint64_t q, uint64_t seed, uint32_t* out_keys, uint32_t* out_expected,
+                                uint8_t* out_present, int32_t device);
+
+/* save_keys / load_keys (keygen.cpp:100-125): flat file of little-endian 32-bit keys.  bht_load_keys sets
+ * *count to the number of keys in the file and copies at most max_keys of them (keys_host may be null). */
+bht_status bht_save_keys(const char* path, const uint32_t* keys_host, uint64_t n);
+bht_status bht_load_keys(const char* path, uint32_t* keys_host, uint64_t max_keys, uint64_t* count);
 
 /* The same bijection / value stream evaluated on the host for one counter / key. */
 uint32_t bht_unique_key_host(uint64_t seed, uint32_t counter);

@@ -429,6 +429,56 @@ class Ref(_Lib):
         self._generate_queries = sig("generate_queries", C.c_int, P32, u64, C.c_double, u64, u64, P32, P32, P8)
         self._hardware_concurrency = sig("hardware_concurrency", C.c_uint)
         self._core_is_reference = sig("core_is_reference", C.c_int)
+        self._has_experiments = sig("has_experiments", C.c_int)
+        if self._has_experiments():
+            dbl, P_D, cp = C.c_double, C.POINTER(C.c_double), C.c_char_p
+            self._config_to_json = sig("config_to_json", C.c_size_t, C.POINTER(Config), cp, C.c_size_t)
+            self._config_from_json = sig("config_from_json", C.c_int, cp, C.POINTER(Config))
+            self._spec_roundtrip = sig("spec_roundtrip", C.c_size_t, cp, cp, C.c_size_t)
+            self._run_experiment = sig("run_experiment", C.c_size_t, cp, C.c_int, cp, C.c_size_t)
+            self._run_trial = sig("run_trial", C.c_int, i32, u32, u32, u64, dbl, P_D, u32, C.c_uint, C.c_uint, u64, P_D)
+            self._run_success_rate = sig("run_success_rate", C.c_int, i32, u32, u32, u64, P_D, u32, C.c_uint, u64, P32)
+
+    # ---- experiment protocol / wire formats (experiments.cpp, core.cpp:70-109) ----
+    def has_experiments(self):
+        return bool(self._has_experiments())
+
+    def _text(self, fn, *args):
+        buf = C.create_string_buffer(1 << 20)
+        n = fn(*args, buf, len(buf))
+        if n == 0:
+            raise ValueError("reference threw")
+        return buf.value.decode()
+
+    def config_to_json(self, cfg):
+        return self._text(self._config_to_json, C.byref(cfg))
+
+    def config_from_json(self, text):
+        cfg = Config()
+        if self._config_from_json(text.encode(), C.byref(cfg)):
+            raise ValueError("config_from_json: invalid")
+        return cfg
+
+    def spec_roundtrip(self, text):
+        return self._text(self._spec_roundtrip, text.encode())
+
+    def run_experiment(self, spec_json, fmt="csv"):
+        return self._text(self._run_experiment, spec_json.encode(), 0 if fmt == "csv" else 1)
+
+    def run_trial(self, kind, b, threshold_pct, n, lf, ratios, trials, max_failures, seed):
+        r = (C.c_double * max(1, len(ratios)))(*ratios)
+        out = (C.c_double * (5 + len(ratios)))()
+        if self._run_trial(kind, b, threshold_pct, n, lf, r, len(ratios), trials, max_failures, seed, out):
+            raise ValueError("run_trial: reference threw")
+        return {"successes": int(out[0]), "failures": int(out[1]), "budget_exhausted": bool(out[2]), "realized_lf": out[3],
+                "insert_mean_probes": out[4], "find_mean_probes": [out[5 + i] for i in range(len(ratios))]}
+
+    def run_success_rate(self, kind, b, threshold_pct, n, lf_grid, success_trials, seed):
+        g = (C.c_double * len(lf_grid))(*lf_grid)
+        succ = (C.c_uint32 * len(lf_grid))()
+        if self._run_success_rate(kind, b, threshold_pct, n, g, len(lf_grid), success_trials, seed, succ):
+            raise ValueError("run_success_rate: reference threw")
+        return [int(x) for x in succ]
 
     def core_is_reference(self):
         return bool(self._core_is_reference())

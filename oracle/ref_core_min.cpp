@@ -48,4 +48,4 @@ table_config make_config(table_kind kind, std::uint64_t n_keys, double lf, std::
 
 }  // namespace bht
 
-extern "C" int ref_core_is_reference() { return 0; }
+extern "C" __attribute__((visibility("default"))) int ref_core_is_reference() { return 0; }

@@ -23,6 +23,11 @@
 #include "bht/oracle.hpp"
 #include "bht/sector_model.hpp"
 #include "bht/table.hpp"
+#ifdef REF_HAS_EXPERIMENTS  // src/experiments.cpp + src/core.cpp need nlohmann/json.hpp (oracle/Makefile)
+#include <sstream>
+
+#include "bht/experiments.hpp"
+#endif
 
 namespace {
 
@@ -79,6 +84,9 @@ struct ref_table {
 
 }  // namespace
 
+// The library is compiled with -fvisibility=hidden so that the reference's (and nlohmann's) inline functions bind
+// inside this .so — a process that also loads torch carries another nlohmann::json with the same symbol names.
+#pragma GCC visibility push(default)
 extern "C" {
 
 std::size_t ref_sizeof_config() { return sizeof(pod_config); }
@@ -315,4 +323,90 @@ std::uint64_t ref_check_admissibility(const ref_table* t) { return bht::check_ad
 
 unsigned ref_hardware_concurrency() { return std::max(1u, std::thread::hardware_concurrency()); }
 
-}  // extern "C"
+
+// ---- experiment protocol and wire formats (experiments.cpp, core.cpp:70-109); 0 when compiled without them ----
+int ref_has_experiments() {
+#ifdef REF_HAS_EXPERIMENTS
+  return 1;
+#else
+  return 0;
+#endif
+}
+
+#ifdef REF_HAS_EXPERIMENTS
+static std::size_t copy_out(const std::string& text, char* buf, std::size_t cap) {
+  if (buf != nullptr && cap != 0) {
+    const std::size_t k = std::min(cap - 1, text.size());
+    std::memcpy(buf, text.data(), k);
+    buf[k] = 0;
+  }
+  return text.size();
+}
+
+// config_to_json; returns the text length (call with a large enough buffer).
+std::size_t ref_config_to_json(const pod_config* cfg, char* buf, std::size_t cap) {
+  return copy_out(bht::config_to_json(to_ref(*cfg)), buf, cap);
+}
+int ref_config_from_json(const char* text, pod_config* out) {
+  try {
+    from_ref(bht::config_from_json(text), out);
+    return 0;
+  } catch (const std::exception&) {
+    return 1;
+  }
+}
+// spec_to_json(spec_from_json(text)): the canonical form of an experiment spec.
+std::size_t ref_spec_roundtrip(const char* text, char* buf, std::size_t cap) {
+  try {
+    return copy_out(bht::spec_to_json(bht::spec_from_json(text)), buf, cap);
+  } catch (const std::exception&) {
+    return 0;
+  }
+}
+// run_experiment(spec_from_json(text)) on the CPU, written with write_csv (format 0) or write_json (format 1).
+std::size_t ref_run_experiment(const char* spec_json, int format, char* buf, std::size_t cap) {
+  try {
+    bht::experiment_result r = bht::run_experiment(bht::spec_from_json(spec_json));
+    std::ostringstream out;
+    if (format == 0) bht::write_csv(out, r); else bht::write_json(out, r);
+    return copy_out(out.str(), buf, cap);
+  } catch (const std::exception&) {
+    return 0;
+  }
+}
+// run_trial: out = {successes, failures, budget_exhausted, realized_lf, insert_mean_probes, find_mean_probes[n_ratios]}
+int ref_run_trial(std::int32_t kind, std::uint32_t b, std::uint32_t threshold_pct, std::uint64_t n, double lf,
+                  const double* ratios, std::uint32_t n_ratios, unsigned trials, unsigned max_failures, std::uint64_t seed,
+                  double* out) {
+  try {
+    bht::trial_cell cell;
+    cell.params = {static_cast<bht::table_kind>(kind), b, threshold_pct};
+    cell.n = n;
+    cell.lf = lf;
+    cell.positive_ratios.assign(ratios, ratios + n_ratios);
+    cell.trials = trials;
+    cell.max_failures = max_failures;
+    cell.seed = seed;
+    bht::trial_outcome o = bht::run_trial(cell);
+    out[0] = o.successes, out[1] = o.failures, out[2] = o.budget_exhausted, out[3] = o.realized_lf, out[4] = o.insert_mean_probes;
+    for (std::uint32_t r = 0; r < n_ratios; ++r) out[5 + r] = o.find_mean_probes[r];
+    return 0;
+  } catch (const std::exception&) {
+    return 1;
+  }
+}
+// run_success_rate: successes per grid point.
+int ref_run_success_rate(std::int32_t kind, std::uint32_t b, std::uint32_t threshold_pct, std::uint64_t n, const double* lf_grid,
+                         std::uint32_t n_lf, unsigned success_trials, std::uint64_t seed, std::uint32_t* successes) {
+  try {
+    auto r = bht::run_success_rate({static_cast<bht::table_kind>(kind), b, threshold_pct}, n,
+                                   std::vector<double>(lf_grid, lf_grid + n_lf), success_trials, seed);
+    for (std::uint32_t i = 0; i < n_lf; ++i) successes[i] = r.points[i].successes;
+    return 0;
+  } catch (const std::exception&) {
+    return 1;
+  }
+}
+#endif
+}
+#pragma GCC visibility pop

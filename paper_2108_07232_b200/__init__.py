@@ -15,6 +15,7 @@ from .table import (  # noqa: E402
     unpack_slot, value_for_key, values_for_keys,
 )
 from ._lib import Config  # noqa: E402
+from . import experiments, workload  # noqa: E402,F401
 from .sharded import ShardedTable, CudaShardOps, shard_constants  # noqa: E402
 
 __all__ = [n for n in dir() if not n.startswith("_")]

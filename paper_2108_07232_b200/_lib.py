@@ -124,6 +124,10 @@ SIGNATURES = {
     "bht_host_alloc": (C.c_int, [C.c_size_t, C.POINTER(_vp)]),
     "bht_host_free": (C.c_int, [_vp]),
     "bht_last_error_string": (C.c_char_p, []),
+    "bht_generate_keys": (C.c_int, [C.c_uint64, C.c_uint64, _vp, C.c_int32, C.c_int32, _vp]),
+    "bht_generate_queries": (C.c_int, [_vp, C.c_uint64, C.c_int32, C.c_double, C.c_uint64, C.c_uint64, _vp, _vp, _vp, C.c_int32]),
+    "bht_save_keys": (C.c_int, [C.c_char_p, _vp, C.c_uint64]),
+    "bht_load_keys": (C.c_int, [C.c_char_p, _vp, C.c_uint64, _u64p]),
     "bht_version_string": (C.c_char_p, []),
     "bht_kernel_launch_count": (C.c_uint64, []),
     "bht_sizeof_config": (C.c_size_t, []),

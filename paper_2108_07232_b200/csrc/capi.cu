@@ -88,6 +88,10 @@ struct Staging {
 
 }  // namespace
 
+namespace bht_b200 {
+void set_last_error(const std::string& msg) { g_error = msg; }  // for the other host TUs (workload.cu)
+}  // namespace bht_b200
+
 struct bht_table {
   bht_config cfg{};
   int device = 0;
@@ -97,7 +101,7 @@ struct bht_table {
   DevCounters* ctr_host = nullptr;  // pinned mirror
   uint32_t* failed_keys = nullptr;  // device log of dropped keys
   // bht_set_blocked_insert: 0 = caller order, 1 = blocked when worth it (default), 2 = always the L2-routed
-  // build, 3 = always the shared-memory-blocked build (cuckoo kinds; other kinds fall back to 2)
+  // build, 3 = always the shared-memory-blocked build (bcht, 8 <= b <= 32; else as 2); bp2ht / iht are never blocked
   int blocked_insert = 1;
   bool known_empty = true;  // no slot has been written since create / clear: a blocked build need not read the store
   // device-resident bht_insert: events around the preparation (routing / binning) and the probe kernel of the last
@@ -257,7 +261,7 @@ uint32_t blocked_regions(const bht_table* t, uint64_t n) {
   // but the balanced placements of bp2ht / iht are order-sensitive: early regions spill into everybody's second
   // choice and the last regions find both candidates full (bp2ht b=16 LF 0.8, 50 M keys: 9302 pairs dropped).
   const bool cuckoo = t->cfg.kind == BHT_BCHT || t->cfg.kind == BHT_ONE_CHT;
-  if (!forced && !cuckoo) return 1;
+  if (!cuckoo) return 1;  // not even when forced: a routed bp2ht / iht build is a different (worse) table
   if (!forced && (n < (4ull << 20) || store_bytes < (192ull << 20))) return 1;
   uint64_t r = (store_bytes + (static_cast<uint64_t>(region_mb) << 20) - 1) / (static_cast<uint64_t>(region_mb) << 20);
   if (forced && r < 4) r = 4;
