@@ -25,7 +25,7 @@ namespace bht_b200 {
 
 // DIRECT selects the register-resident probe (direct_load) instead of the shared-memory staged one.
 template <int B, int H, bool DIRECT>
-__global__ void __launch_bounds__(block_threads<B>(1), DIRECT ? 3 : 6)
+__global__ void __launch_bounds__(block_threads<B>(1), DIRECT ? 5 : 6)
 bulk_insert_cuckoo_kernel(const __grid_constant__ TableView t, const PairSource src, uint64_t n,
                           const unsigned long long* __restrict__ n_dev, const bool routed,
                           DevCounters* __restrict__ ctr, uint32_t* __restrict__ failed_keys, uint64_t failed_cap,

@@ -163,9 +163,9 @@ __device__ __forceinline__ uint32_t staged_prefix_load(uint32_t base) {
 
 // ---- direct load (insert side, register-resident) ------------------------------------------------
 // The bucket never touches shared memory: the C = B/2 lanes of a tile read one bucket with one 16-byte
-// LDG each (iteration u of a tile serves the key of the tile's u-th lane), count their empty slots and
-// add the counts up inside the tile (two ballots + popc).  load = B - empties (occupied slots form a prefix,
-// see staged_prefix_load).  No LDGSTS shared-memory write, no LDS: less work for the SM's load/store
+// LDG each (iteration u of a tile serves the key of the tile's u-th lane), count their occupied slots and
+// add the counts up inside the tile (packed bytes + shuffle butterfly).  load = occupied slots (they form a
+// prefix, see staged_prefix_load).  No LDGSTS shared-memory write, no LDS: less work for the SM's load/store
 // pipe than the staged engine, at the price of B/2 x 4 registers held while the lines are in flight —
 // the trade that pays when the probes are L2-resident and few keys in flight suffice (routed builds).
 template <int B>
@@ -174,7 +174,6 @@ __device__ __forceinline__ uint32_t direct_load(const uint64_t* __restrict__ sto
   constexpr int C = B / 2;
   const int sub = lane & (C - 1);
   const int tile_base = lane & ~(C - 1);
-  constexpr uint32_t kTileBits = (1u << C) - 1u;
   uint4 v[C];
 #pragma unroll
   for (int u = 0; u < C; ++u) {
@@ -182,15 +181,23 @@ __device__ __forceinline__ uint32_t direct_load(const uint64_t* __restrict__ sto
     v[u] = make_uint4(0u, 0u, 0u, 0u);
     if (bid != kNoBucket) v[u] = ldg_whole_v4(store + static_cast<uint64_t>(bid) * B + sub * 2);
   }
-  uint32_t empties = 0;
+  // Occupied slots seen by this lane in iteration u go to byte u % 4 of acc[u / 4]; a butterfly over the C lanes of
+  // the tile then adds the bytes up for all C keys at once (a byte never exceeds B <= 16, so nothing carries):
+  // log2(C) shuffles per accumulator instead of two ballots + two popcounts per key.
+  uint32_t acc[(C + 3) / 4] = {};
 #pragma unroll
   for (int u = 0; u < C; ++u) {
-    const uint32_t e0 = __ballot_sync(kFullMask, v[u].x == kEmptyKey) >> tile_base;
-    const uint32_t e1 = __ballot_sync(kFullMask, v[u].z == kEmptyKey) >> tile_base;
-    const uint32_t s = __popc(e0 & kTileBits) + __popc(e1 & kTileBits);
-    if (sub == u) empties = s;
+    const uint32_t occ = (v[u].x != kEmptyKey) + (v[u].z != kEmptyKey);
+    acc[u / 4] += occ << (8 * (u % 4));
   }
-  return B - empties;
+#pragma unroll
+  for (int a = 0; a < (C + 3) / 4; ++a) {
+#pragma unroll
+    for (int o = 1; o < C; o <<= 1) acc[a] += __shfl_xor_sync(kFullMask, acc[a], o);
+  }
+  uint32_t mine = acc[0];
+  if constexpr (C > 4) mine = sub < 4 ? acc[0] : acc[1];
+  return (mine >> (8 * (sub & 3))) & 0xFFu;
 }
 
 // ---- scan -------------------------------------------------------------------------------------

@@ -139,3 +139,29 @@ def test_key_file_round_trip_and_byte_order(bht, ref, tmp_path):
         workload.load_keys(str(tmp_path / "missing.bin"))
     with pytest.raises(OSError):
         workload.save_keys(str(tmp_path / "no_such_dir" / "k.bin"), keys)
+
+
+# ---- committed fixtures (tests/golden/reference_formats.json, made by tests/golden/make_golden_workload.py) ----------
+
+GOLDEN_FORMATS = os.path.join(os.path.dirname(__file__), "golden", "reference_formats.json")
+
+
+def test_golden_config_json_and_csv(bht, ex):
+    """The same pins without oracle/_ref: config JSON text per (kind, n, lf, b, t, seed), and the reference's CSV of one
+    tiny run reproduced by write_csv from its own parsed records (ops_per_sec column aside)."""
+    doc = json.load(open(GOLDEN_FORMATS))
+    for case in doc["configs"]:
+        kind, n, lf, b, t, seed = case["args"]
+        assert ex.config_to_json(bht.make_config(kind, n, lf, b, threshold=t, seed=seed)) == case["json"]
+        assert ex.config_to_json(ex.config_from_json(case["json"])) == case["json"]
+    recs = parse_reference_csv(ex, doc["csv"])
+    assert [r.op for r in recs[:3]] == ["insert", "find", "find"] and recs[0].positive_ratio is None
+    assert all(r.threshold_pct == (75 if r.kind == "iht" else None) for r in recs)
+    out = io.StringIO()
+    ex.write_csv(out, ex.ExperimentResult(recs))
+    assert out.getvalue() == doc["csv"]          # ops_per_sec too: '%.6g' of the parsed double is the same text
+    spec = ex.spec_from_json(json.dumps(doc["spec"]))
+    assert (spec.trials, spec.max_failures, spec.seed, [k.threshold_pct for k in spec.kinds]) == (2, 5, 42, [80, 75])
+    mine = io.StringIO()
+    ex.write_json(mine, ex.ExperimentResult(recs[:1]))
+    assert sorted(json.loads(mine.getvalue())["records"][0]) == doc["result_json_members"]

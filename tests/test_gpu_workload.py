@@ -44,6 +44,17 @@ def test_generate_keys_golden_fixture(wl):
         assert np.array_equal(got, keys)
 
 
+def test_workload_golden_fixture(wl):
+    """tests/golden/workload_vectors.npz (made from the reference by tests/golden/make_golden_workload.py)."""
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "workload_vectors.npz"))
+    for i, seed in enumerate(g["keys_seed"]):
+        assert np.array_equal(wl.generate_keys(int(seed), 5000, device=0).keys.cpu().numpy(), g[f"keys_{i}"])
+    for i, (n, q, pct, seed) in enumerate(g["query_cases"]):
+        keys = wl.generate_keys(int(seed) + 100, int(n), device=0)
+        got = wl.generate_queries(keys, int(pct) / 100.0, int(q), int(seed), device=0)
+        assert np.array_equal(got.keys, g[f"q{i}_keys"]) and np.array_equal(got.expected_present, g[f"q{i}_present"])
+
+
 def test_generate_keys_with_many_duplicates_in_the_stream(wl, ref):
     """50 M draws of a 32-bit stream repeat ~290 k values: first occurrence wins, order preserved, top-up batches
     continue the same stream (checked through a position-weighted checksum against the reference's own output)."""
