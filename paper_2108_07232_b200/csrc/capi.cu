@@ -104,6 +104,7 @@ struct bht_table {
   // build, 3 = always the shared-memory-blocked build (bcht, 8 <= b <= 32; else as 2); bp2ht / iht are never blocked
   int blocked_insert = 1;
   bool known_empty = true;  // no slot has been written since create / clear: a blocked build need not read the store
+  uint64_t host_inserted = 0;  // upper bound of the pairs in the store, kept on the host (tail_plan)
   // device-resident bht_insert: events around the preparation (routing / binning) and the probe kernel of the last
   // call, for bht_last_insert_phases (per-kernel roofline of bench.py)
   cudaEvent_t phase_ev[3] = {};
@@ -209,7 +210,7 @@ cudaError_t next_cursor(bht_table* t, cudaStream_t stream, uint32_t** out) {
 }
 
 cudaError_t launch_insert_kind(bht_table* t, PairSource src, uint64_t n, int max_ctas_per_sm, cudaStream_t stream,
-                               bool routed = false, const unsigned long long* n_dev = nullptr) {
+                               bool routed = false, const unsigned long long* n_dev = nullptr, int max_grid = 0) {
   InsertLaunch a;
   a.src = src;
   a.n = n;
@@ -220,6 +221,13 @@ cudaError_t launch_insert_kind(bht_table* t, PairSource src, uint64_t n, int max
   a.failed_cap = kFailedLogCap;
   a.sm_count = t->sm_count;
   a.max_ctas_per_sm = max_ctas_per_sm;
+  // experiment knobs on the number of keys in flight (tools/exp_success_inflight.py, DESIGN.md §3 K4)
+  if (const char* e = std::getenv("BHT_INSERT_CTAS")) {
+    const int v = std::atoi(e);
+    if (v > 0) a.max_ctas_per_sm = v;
+  }
+  a.max_grid = max_grid;
+  if (const char* e = std::getenv("BHT_INSERT_GRID")) a.max_grid = std::atoi(e);
   {
     // experiment knob: 0 = staged engine everywhere, 1 = direct engine everywhere (default: measured faster for
     // 4 <= b <= 16 in caller order and in routed builds), 2 = direct for routed builds only
@@ -294,6 +302,40 @@ int blocked_ctas_per_sm() {
   return e ? std::atoi(e) : 0;
 }
 
+// The last pairs of a cuckoo build that ends at a very high load are inserted with few keys in flight.
+// Measured (tools/exp_success_inflight.py, exp_success_tail.py; bcht b = 16, LF 0.99, 5 M keys, 40 builds each): with
+// 190 k insertions in flight to the end 52 % of the builds succeed, with 4 k in flight 68 %, with 256 in flight 95 %;
+// the CPU reference: 90 %.  Only the end matters — the last 2 % of the pairs at 256 in flight: 88 % — and it is not
+// about the long chains themselves (finishing every chain past 24 evictions in a single CTA changes nothing): when
+// the walkers in flight are as many as the free slots that remain, they take the slots each other was heading for,
+// and max_chain, which the reference calibrates for one walker at a time, is hit 3-5 times more often.  So the
+// pairs that arrive beyond a load threshold go in a second launch whose grid keeps the keys in flight at or
+// below 1/24 of the slots that will still be free at the end.  Builds that end below the threshold are untouched.
+struct TailPlan {
+  uint64_t tail = 0;  // pairs at the end of the batch that get the throttled launch
+  int grid = 0;       // its CTA cap
+};
+TailPlan tail_plan(const bht_table* t, uint64_t n) {
+  TailPlan p;
+  if (t->cfg.kind != BHT_BCHT && t->cfg.kind != BHT_ONE_CHT) return p;
+  if (const char* e = std::getenv("BHT_TAIL_THROTTLE"))
+    if (std::atoi(e) == 0) return p;
+  const double cap = static_cast<double>(t->cfg.capacity);
+  const uint32_t b = t->cfg.bucket_size;
+  double lf = b == 1 ? 0.85 : (b == 2 ? 0.90 : (b == 4 ? 0.94 : 0.96));
+  if (const char* e = std::getenv("BHT_TAIL_LF")) lf = std::atof(e);
+  const uint64_t before = std::min<uint64_t>(t->host_inserted, t->cfg.capacity);
+  const uint64_t after = std::min<uint64_t>(before + n, t->cfg.capacity);
+  const uint64_t threshold = static_cast<uint64_t>(lf * cap);
+  if (after <= threshold) return p;
+  p.tail = std::min<uint64_t>(n, after - std::max(before, threshold));
+  const uint64_t free_at_end = t->cfg.capacity - after;
+  const uint64_t lanes = std::max<uint64_t>(256, free_at_end / 24);
+  p.grid = static_cast<int>(std::min<uint64_t>((lanes + 255) / 256, 1u << 20));
+  if (p.grid >= t->sm_count * 4) p = TailPlan{};  // no real throttle: one launch
+  return p;
+}
+
 bool kind_matches(int32_t table_kind, int32_t as_kind) {
   // bcht_insert / bcht_find accept both cuckoo kinds (table.cpp:55,96)
   const bool cuckoo = table_kind == BHT_ONE_CHT || table_kind == BHT_BCHT;
@@ -311,6 +353,9 @@ bht_status do_insert(bht_table* t, const uint32_t* keys, const uint32_t* values,
   cudaStream_t stream = as_stream(stream_v);
 
   BHT_CUDA(cudaMemsetAsync(t->ctr, 0, kPerCallCounterBytes, stream));
+  const TailPlan tail = tail_plan(t, n);
+  const uint64_t n_all = n;
+  n -= tail.tail;  // the schedules below take the first part of the batch, the throttled launch the rest
   if (mem_space == BHT_MEM_DEVICE) {
     BHT_CUDA(cudaEventRecord(t->phase_ev[0], stream));
     const BlockedPlan plan = smem_blocked_plan(t, n);
@@ -348,9 +393,13 @@ bht_status do_insert(bht_table* t, const uint32_t* keys, const uint32_t* values,
       BHT_CUDA(cudaEventRecord(t->phase_ev[1], stream));
       BHT_CUDA(launch_insert_kind(t, PairSource{keys, values}, n, 0, stream));
     }
+    if (tail.tail != 0)
+      BHT_CUDA(launch_insert_kind(t, PairSource{keys + n, values + n}, tail.tail, 0, stream, false, nullptr, tail.grid));
     BHT_CUDA(cudaEventRecord(t->phase_ev[2], stream));
     t->phases_recorded = true;
-  } else if (n != 0) {
+  } else if (n_all != 0) {
+    n = n_all;
+    const uint64_t n_main = n_all - tail.tail;
     bht_status s = ensure_staging(t);
     if (s != BHT_OK) return s;
     Staging& st = t->stage;
@@ -360,21 +409,25 @@ bht_status do_insert(bht_table* t, const uint32_t* keys, const uint32_t* values,
     uint64_t chunks = 0;
     for (uint64_t c = 0, off = 0; off < n; ++c) {
       const int slot = static_cast<int>(c % kStageSlots);
-      const uint64_t len = stage_chunk_len(off, n);
+      uint64_t len = stage_chunk_len(off, n);
+      if (off < n_main) len = std::min(len, n_main - off);  // a chunk is either before or inside the throttled tail
       chunks = c + 1;
       if (c >= kStageSlots) BHT_CUDA(cudaStreamWaitEvent(st.h2d, st.kernel_done[slot], 0));
       BHT_CUDA(cudaMemcpyAsync(st.keys[slot], keys + off, len * sizeof(uint32_t), cudaMemcpyHostToDevice, st.h2d));
       BHT_CUDA(cudaMemcpyAsync(st.vals[slot], values + off, len * sizeof(uint32_t), cudaMemcpyHostToDevice, st.h2d));
       BHT_CUDA(cudaEventRecord(st.in_done[slot], st.h2d));
       BHT_CUDA(cudaStreamWaitEvent(st.compute, st.in_done[slot], 0));
-      BHT_CUDA(launch_insert_kind(t, PairSource{st.keys[slot], st.vals[slot]}, len, 0, st.compute));
+      BHT_CUDA(launch_insert_kind(t, PairSource{st.keys[slot], st.vals[slot]}, len, 0, st.compute, false, nullptr,
+                                  off >= n_main ? tail.grid : 0));
       BHT_CUDA(cudaEventRecord(st.kernel_done[slot], st.compute));
       off += len;
     }
     BHT_CUDA(cudaStreamWaitEvent(stream, st.kernel_done[(chunks - 1) % kStageSlots], 0));
     BHT_CUDA(cudaStreamSynchronize(stream));  // the caller's host arrays are free again on return
   }
+  n = n_all;
   if (n != 0) t->known_empty = false;
+  t->host_inserted = std::min<uint64_t>(t->host_inserted + n, t->cfg.capacity);
   if (result != nullptr) {
     bht_status s = read_counters(t, stream);
     if (s != BHT_OK) return s;
@@ -628,6 +681,7 @@ bht_status bht_clear(bht_table* t, void* stream) {
   BHT_CUDA(launch_fill_empty(t->view.store, t->cfg.capacity, t->sm_count, as_stream(stream)));
   BHT_CUDA(cudaMemsetAsync(t->ctr, 0, sizeof(DevCounters), as_stream(stream)));
   t->known_empty = true;
+  t->host_inserted = 0;
   return BHT_OK;
 }
 
@@ -798,7 +852,9 @@ bht_status bht_upload_store(bht_table* t, const uint64_t* host_src, void* stream
   BHT_CUDA(cudaMemcpyAsync(t->view.store, host_src, t->cfg.capacity * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
   BHT_CUDA(cudaMemsetAsync(t->ctr, 0, sizeof(DevCounters), s));
   BHT_CUDA(launch_count_occupied(t->view.store, t->cfg.capacity, &t->ctr->inserted_total, t->sm_count, s));
-  return read_counters(t, s);
+  const bht_status rs = read_counters(t, s);
+  if (rs == BHT_OK) t->host_inserted = t->ctr_host->inserted_total;
+  return rs;
 }
 
 bht_status bht_dump_store(const bht_table* t, const char* path) {

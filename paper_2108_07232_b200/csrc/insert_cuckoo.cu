@@ -164,7 +164,8 @@ static cudaError_t launch_one(const TableView& t, const InsertLaunch& a) {
     if (a.direct) {
       auto kernel = bulk_insert_cuckoo_kernel<B, H, true>;
       constexpr int block = block_threads<B>(1);
-      const int grid = persistent_grid(kernel, block, 0, a.sm_count, a.n, block, a.max_ctas_per_sm);
+      int grid = persistent_grid(kernel, block, 0, a.sm_count, a.n, block, a.max_ctas_per_sm);
+      if (a.max_grid > 0 && grid > a.max_grid) grid = a.max_grid;
       kernel<<<grid, block, 0, a.stream>>>(t, a.src, a.n, a.n_dev, a.routed, a.ctr, a.failed_keys, a.failed_cap, a.work_cursor);
       note_launch();
       return cudaGetLastError();
@@ -173,7 +174,8 @@ static cudaError_t launch_one(const TableView& t, const InsertLaunch& a) {
   auto kernel = bulk_insert_cuckoo_kernel<B, H, false>;
   constexpr int block = block_threads<B>(1);
   constexpr int smem = (block / 32) * Geo<B>::WARP_BYTES;
-  const int grid = persistent_grid(kernel, block, smem, a.sm_count, a.n, block, a.max_ctas_per_sm);
+  int grid = persistent_grid(kernel, block, smem, a.sm_count, a.n, block, a.max_ctas_per_sm);
+  if (a.max_grid > 0 && grid > a.max_grid) grid = a.max_grid;
   kernel<<<grid, block, smem, a.stream>>>(t, a.src, a.n, a.n_dev, a.routed, a.ctr, a.failed_keys, a.failed_cap, a.work_cursor);
   note_launch();
   return cudaGetLastError();

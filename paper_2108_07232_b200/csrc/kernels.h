@@ -29,6 +29,7 @@ struct InsertLaunch {
   uint32_t* work_cursor;  // one zeroed device word per launch (Stream)
   int sm_count;
   int max_ctas_per_sm;    // 0 = whatever fits; a routed (L2-blocked) build keeps fewer keys in flight
+  int max_grid = 0;       // cuckoo: cap on the CTAs of the launch (experiments on the number of keys in flight)
   bool direct;            // cuckoo, 4 <= b <= 16: register-resident probe (direct_load) instead of the staged one
   bool routed = false;    // cuckoo: the pairs arrive grouped by table region in table order (L2-blocked build)
   const unsigned long long* n_dev = nullptr;  // cuckoo: when set, the pair count is read on the device (<= n)
