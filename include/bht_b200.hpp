@@ -139,6 +139,14 @@ class hash_table {
   }
   void clear(void* stream = nullptr) { check(bht_clear(h_, stream)); }
   void set_iht_prose_fallback(bool on) { check(bht_set_iht_prose_fallback(h_, on ? 1 : 0)); }
+  // bulk-build schedule: 0 caller order, 1 blocked when it pays (default), 2 L2-routed, 3 shared-memory blocked
+  void set_blocked_insert(int mode) { check(bht_set_blocked_insert(h_, mode)); }
+  // device milliseconds of the last device-resident insert: {routing / binning passes, probe kernel}
+  std::pair<float, float> last_insert_phases() {
+    float prepare = 0.f, probe = 0.f;
+    check(bht_last_insert_phases(h_, &prepare, &probe));
+    return {prepare, probe};
+  }
 
   // bulk insert_pair (table.hpp:103-104)
   build_outcome insert(const key_type* keys, const value_type* values, std::uint64_t n, mem_space space = mem_space::host,
@@ -253,6 +261,129 @@ inline std::pair<hash_table, build_outcome> build_pairs(const key_type* keys, co
   check(bht_build(&cfg, opts.device, keys, values, n, static_cast<std::int32_t>(opts.space), opts.iht_prose_fallback ? 1 : 0, &h, &r,
                   opts.stream));
   return {hash_table(h, cfg), hash_table::outcome_of(r)};
+}
+
+// ---- workload (keygen.hpp) ------------------------------------------------------------------------------------
+
+struct key_set {  // keygen.hpp:13-18
+  std::vector<key_type> keys;
+  std::uint64_t seed = 0;
+  std::size_t size() const { return keys.size(); }
+};
+struct query {  // keygen.hpp:30-34
+  key_type key = 0;
+  value_type expected_value = 0;
+  bool expected_present = false;
+};
+
+// generate_keys (keygen.cpp:50-64): the reference's stream, de-duplicated on the device.
+inline key_set generate_keys(std::uint64_t seed, std::size_t n, int device = 0) {
+  key_set out;
+  out.seed = seed;
+  out.keys.resize(n);
+  check(bht_generate_keys(seed, n, out.keys.data(), BHT_MEM_HOST, device, nullptr));
+  return out;
+}
+// generate_queries (keygen.cpp:66-98); throws std::invalid_argument like the reference.
+inline std::vector<query> generate_queries(const key_set& keys, double positive_ratio, std::size_t q, std::uint64_t seed,
+                                           int device = 0) {
+  std::vector<key_type> k(q);
+  std::vector<value_type> v(q);
+  std::vector<std::uint8_t> p(q);
+  check(bht_generate_queries(keys.keys.data(), keys.size(), BHT_MEM_HOST, positive_ratio, q, seed, k.data(), v.data(), p.data(), device));
+  std::vector<query> out(q);
+  for (std::size_t i = 0; i < q; ++i) out[i] = {k[i], v[i], p[i] != 0};
+  return out;
+}
+inline void save_keys(const std::string& path, const key_set& keys) { check(bht_save_keys(path.c_str(), keys.keys.data(), keys.size())); }
+inline key_set load_keys(const std::string& path, std::uint64_t seed) {
+  key_set out;
+  out.seed = seed;
+  std::uint64_t count = 0;
+  check(bht_load_keys(path.c_str(), nullptr, 0, &count));
+  out.keys.resize(count);
+  check(bht_load_keys(path.c_str(), out.keys.data(), count, &count));
+  return out;
+}
+
+// ---- the trial protocol (experiments.hpp:84-113, experiments.cpp:51-112) ----------------------------------------
+
+struct kind_params {
+  table_kind kind = table_kind::bcht;
+  std::uint32_t bucket_size = 16;
+  std::uint32_t threshold_pct = 80;  // iht only
+  std::optional<std::uint32_t> threshold_slots() const {
+    if (kind != table_kind::iht) return std::nullopt;
+    return bucket_size * threshold_pct / 100;
+  }
+};
+struct trial_cell {
+  kind_params params;
+  std::uint64_t n = 0;
+  double lf = 0.0;
+  std::vector<double> positive_ratios;
+  unsigned trials = 10;
+  unsigned max_failures = 50;
+  std::uint64_t seed = 0;
+  build_options build_opts;
+  std::optional<std::uint32_t> max_chain;
+  const key_set* preloaded_keys = nullptr;
+};
+struct trial_outcome {
+  unsigned successes = 0;
+  unsigned failures = 0;
+  bool budget_exhausted = false;
+  double realized_lf = 0.0;
+  double insert_mean_probes = 0.0;
+  std::vector<double> find_mean_probes;  // parallel to the requested ratios
+};
+
+// run_trial: fresh hash constants per attempt (mix_seed(seed, 0x100 + attempt)), build until `trials` successes or the
+// failure budget runs out; on each success one bulk find of q = n queries per ratio (mix_seed(seed, 0x200 + r)).
+inline trial_outcome run_trial(const trial_cell& cell) {
+  trial_outcome out;
+  out.find_mean_probes.assign(cell.positive_ratios.size(), 0.0);
+  key_set local;
+  const key_set* keys = cell.preloaded_keys;
+  if (keys == nullptr || keys->size() != cell.n) {
+    local = generate_keys(mix_seed(cell.seed, 0x6b657973ull), cell.n, cell.build_opts.device);
+    keys = &local;
+  }
+  std::uint64_t ins_probes = 0, ins_ops = 0;
+  std::vector<std::uint64_t> find_probes(cell.positive_ratios.size(), 0), find_ops(cell.positive_ratios.size(), 0);
+  std::vector<std::vector<key_type>> queries(cell.positive_ratios.size());
+  std::vector<value_type> answers(cell.n);
+  unsigned attempt = 0;
+  while (out.successes < cell.trials && out.failures < cell.max_failures) {
+    table_config cfg = make_config(cell.params.kind, cell.n, cell.lf, cell.params.bucket_size, cell.params.threshold_slots(),
+                                   mix_seed(cell.seed, 0x100 + attempt), cell.max_chain);
+    ++attempt;
+    out.realized_lf = static_cast<double>(cell.n) / static_cast<double>(cfg.capacity);
+    auto [table, built] = build(keys->keys.data(), cell.n, cfg, cell.build_opts);
+    if (!built.success) {
+      ++out.failures;
+      continue;
+    }
+    ++out.successes;
+    ins_probes += built.probes;
+    ins_ops += built.attempted;
+    for (std::size_t r = 0; r < cell.positive_ratios.size(); ++r) {
+      if (queries[r].empty() && cell.n != 0) {
+        for (const query& qu : generate_queries(*keys, cell.positive_ratios[r], cell.n, mix_seed(cell.seed, 0x200 + r),
+                                                cell.build_opts.device))
+          queries[r].push_back(qu.key);
+      }
+      find_stats fs;
+      table.find(queries[r].data(), answers.data(), cell.n, mem_space::host, nullptr, &fs);
+      find_probes[r] += fs.probes;
+      find_ops[r] += fs.queries;
+    }
+  }
+  out.budget_exhausted = out.successes < cell.trials;
+  out.insert_mean_probes = ins_ops ? static_cast<double>(ins_probes) / static_cast<double>(ins_ops) : 0.0;
+  for (std::size_t r = 0; r < cell.positive_ratios.size(); ++r)
+    out.find_mean_probes[r] = find_ops[r] ? static_cast<double>(find_probes[r]) / static_cast<double>(find_ops[r]) : 0.0;
+  return out;
 }
 
 }  // namespace gpu

@@ -94,6 +94,71 @@ int main(int argc, char** argv) {
   table_config bad = small;
   bad.n_hashes = 2;
   CHECK(throws<std::invalid_argument>([&] { hash_table t(bad); }));
+  // workload generators: the same stream as std::mt19937_64 + first-occurrence rejection (keygen.cpp:50-64)
+  {
+    const std::size_t m = 50000;
+    key_set ks = generate_keys(7, m);
+    std::mt19937_64 eng(7);
+    std::unordered_set<key_type> dedupe;
+    std::vector<key_type> want;
+    while (want.size() < m) {
+      key_type k = static_cast<key_type>(eng() >> 32);
+      if (k == empty_key || !dedupe.insert(k).second) continue;
+      want.push_back(k);
+    }
+    CHECK(ks.keys == want && ks.seed == 7);
+    auto qs = generate_queries(ks, 0.5, 1000, 5);
+    std::size_t positives = 0;
+    for (const query& q : qs) {
+      positives += q.expected_present;
+      CHECK(q.expected_present == (dedupe.count(q.key) != 0));
+      if (q.expected_present) CHECK(q.expected_value == value_for_key(q.key));
+    }
+    CHECK(qs.size() == 1000 && positives == 500);  // test_keygen.cpp:64-69
+    CHECK(throws<std::invalid_argument>([&] { generate_queries(ks, 1.1, 10, 1); }));
+    CHECK(throws<std::invalid_argument>([&] { generate_queries(ks, 1.0, m + 1, 1); }));
+    save_keys("keys_roundtrip.bin", ks);  // test_keygen.cpp:78-86
+    CHECK(load_keys("keys_roundtrip.bin", ks.seed).keys == ks.keys);
+    std::remove("keys_roundtrip.bin");
+    CHECK(throws<std::runtime_error>([] { load_keys("/nonexistent/dir/keys.bin", 0); }));
+  }
+  // trial protocol (test_experiments.cpp:113-138)
+  {
+    trial_cell cell;
+    cell.params = {table_kind::bcht, 16, 80};
+    cell.n = 10000;
+    cell.lf = 0.1;
+    cell.trials = 3;
+    cell.seed = 7;
+    cell.positive_ratios = {1.0, 0.0};
+    trial_outcome o = run_trial(cell);
+    CHECK(o.successes == 3 && o.failures == 0 && !o.budget_exhausted);
+    CHECK(o.insert_mean_probes == 1.0 && o.find_mean_probes[0] == 1.0 && o.find_mean_probes[1] == 1.0);
+    trial_cell hard;
+    hard.params = {table_kind::bp2ht, 8, 80};
+    hard.n = 10000;
+    hard.lf = 1.0;
+    hard.trials = 1;
+    hard.max_failures = 5;
+    hard.seed = 7;
+    trial_outcome h = run_trial(hard);
+    CHECK(h.budget_exhausted && h.successes == 0 && h.failures == 5);
+  }
+  // set_blocked_insert is part of the handle API (host batches are always staged in caller order; the device-resident
+  // schedules are covered by tests/test_gpu_parity.py::test_build_parity_routed)
+  {
+    table_config cfg = make_config(table_kind::bcht, n, 0.9, 16, std::nullopt, 9);
+    for (int mode : {0, 2, 3}) {
+      hash_table t(cfg);
+      t.set_blocked_insert(mode);
+      std::vector<value_type> vals(n), out(n);
+      for (std::uint64_t i = 0; i < n; ++i) vals[i] = value_for_key(keys[i]);
+      build_outcome o = t.insert(keys.data(), vals.data(), n);
+      CHECK(o.success && t.count_inadmissible() == 0);
+      t.find(keys.data(), out.data(), n);
+      CHECK(out == vals);
+    }
+  }
   std::puts("wrapper checks ok");
   return 0;
 }
