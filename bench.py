@@ -32,8 +32,18 @@ KIND, B, LF, N_KEYS, SEED = "bcht", 16, 0.9, 50_000_000, 1
 METRIC = "insert & find MKeys/s, BCHT b=16, 50M keys, LF 0.9"
 
 
+KEYS_STREAM, QUERY_STREAM = 0x6B657973, 0x200  # the reference harness's seed streams (experiments.cpp:59,88-89)
+
+
+def make_values(n: int, seed: int):
+    """n sentinel-free u32 values from a second MT19937 stream."""
+    rng = np.random.Generator(np.random.MT19937(seed ^ 0x76616C73))
+    v = rng.integers(0, 0xFFFFFFFF, size=n, dtype=np.uint32)  # high is exclusive: never the sentinel
+    return v
+
+
 def make_workload(n: int, seed: int):
-    """n present + n absent unique sentinel-free u32 keys and n values from MT19937 streams (uniform, random order)."""
+    """(--workload numpy) n present + n absent unique sentinel-free u32 keys and n values from MT19937 streams."""
     rng = np.random.Generator(np.random.MT19937(seed))
     raw = rng.integers(0, 0xFFFFFFFF, size=int(2 * n * 1.02) + 1024, dtype=np.uint32)
     raw.sort()
@@ -132,7 +142,10 @@ def run_reference(args):
     ref = binding.ref()
     threads = ref.hardware_concurrency()
     n = args.keys
-    present, _absent, _values = make_workload(n, SEED)
+    if args.workload == "reference":
+        present = ref.generate_keys(ref.mix_seed(SEED, KEYS_STREAM), n)  # the harness's own key set (experiments.cpp:59)
+    else:
+        present, _absent, _values = make_workload(n, SEED)
     ocfg = make_ref_config(ref, n)
     # size the per-step sample so that the whole run ends within a few minutes
     t0 = time.time()
@@ -159,7 +172,7 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": value, "unit": "MKeys/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32/u64 integer",
-        "data": "synthetic: unique uniform u32 keys, MT19937",
+        "data": data_label(args),
         "config": workload_config(n, args.gpus, ocfg.capacity * 8 / 1e6),
         "cpu_baseline": {"value": value, "unit": "MKeys/s", "cores": threads, "kind": "reference", "sample": sample,
                          "insert_mkeys": n_sample * args.steps / sum(tbs) / 1e6,
@@ -175,6 +188,13 @@ def make_ref_config(ref, n):
     from oracle import binding
     cfg = ref.make_config(binding.KINDS[KIND], n, LF, B, seed=ref.mix_seed(SEED, 0x100))
     return cfg
+
+
+def data_label(args):
+    if args.workload == "reference":
+        return ("synthetic: the reference harness's workload for seed 1 - generate_keys (unique uniform u32, mt19937_64) and "
+                "generate_queries per positive ratio; values from a second MT19937 stream")
+    return "synthetic: unique uniform u32 keys, MT19937"
 
 
 def workload_config(n, gpus, table_mb=None):
@@ -234,6 +254,21 @@ def run_cuda(args):
             da = bht.generate_unique_keys(SEED, n, n, device=local, with_values=False)
             d_keys, d_vals, d_abs = dk.view(torch.int32), dv.view(torch.int32), da.view(torch.int32)
             present, values, absent = None, None, None
+        elif args.workload == "reference":
+            # exactly what the reference's run_trial would build and query for seed S = 1 (experiments.cpp:59,88-89),
+            # generated through this library (element for element the reference's outputs, tests/test_gpu_workload.py)
+            ks = bht.workload.generate_keys(bht.mix_seed(SEED, KEYS_STREAM), n, device=local)
+            d_keys = ks.keys.view(torch.int32)
+            present = d_keys.cpu().numpy().view(np.uint32)
+            values = make_values(n, SEED)
+            d_vals = torch.from_numpy(values.view(np.int32)).to(device)
+            qsets = []
+            for r, ratio in enumerate((1.0, 0.5, 0.0)):
+                q = bht.workload.generate_queries(ks, ratio, n, bht.mix_seed(SEED, QUERY_STREAM + r), device=local)
+                assert int(q.expected_present.sum()) == int(round(ratio * n))
+                qsets.append(torch.from_numpy(q.keys.view(np.int32)).to(device))
+            d_pos, d_mixed, d_abs = qsets
+            absent = None
         else:
             present, absent, values = make_workload(n, SEED)
             d_keys = torch.from_numpy(present.view(np.int32)).to(device)
@@ -241,7 +276,9 @@ def run_cuda(args):
             d_abs = torch.from_numpy(absent.view(np.int32)).to(device)
         d_out = torch.empty(n, dtype=torch.int32, device=device)
         half = n // 2
-        d_mixed = torch.cat([d_keys[:half], d_abs[:n - half]])[torch.randperm(n, device=device)].contiguous()
+        if args.device_keys or args.workload != "reference":
+            d_pos = d_keys
+            d_mixed = torch.cat([d_keys[:half], d_abs[:n - half]])[torch.randperm(n, device=device)].contiguous()
         table = bht.HashTable(cfg, local)
 
         def step(timers=None):
@@ -251,7 +288,7 @@ def run_cuda(args):
             if e: e[1].record(stream)
             table.insert(d_keys, d_vals, want_result=False)
             if e: e[2].record(stream)
-            table.find(d_keys, d_out)
+            table.find(d_pos, d_out)
             if e: e[3].record(stream)
             if timers is not None:
                 timers.append(e)
@@ -281,7 +318,7 @@ def run_cuda(args):
 
         # probe counts of this very workload (device counters = probe_stats, probe_stats.hpp:12-31)
         outcome = table.last_insert_result()
-        _, fs100 = table.find(d_keys, d_out, want_stats=True)
+        _, fs100 = table.find(d_pos, d_out, want_stats=True)
         assert fs100.hits == n
         checksum_ok = fs100.value_sum == int((d_vals.to(torch.int64) & 0xFFFFFFFF).sum().item())
         assert checksum_ok, "find checksum mismatch"
@@ -301,7 +338,7 @@ def run_cuda(args):
         f0_ms = timed_find(d_abs)
         _, fs50 = table.find(d_mixed, d_out, want_stats=True)
         _, fs0 = table.find(d_abs, d_out, want_stats=True)
-        assert fs0.hits == 0 and fs50.hits == half
+        assert fs0.hits == 0 and fs50.hits == int(round(0.5 * n))
 
         # the insert op = routing passes + the bulk-insert kernel: time the kernel alone (events inside the library)
         prep, probe = [], []
@@ -374,7 +411,7 @@ def run_cuda(args):
             "metric": METRIC, "value": value, "unit": "MKeys/s", "n_gpus": 1, "steps": args.steps,
             "warmup": max(args.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u32/u64 integer", "data": ("synthetic: unique u32 keys from the device bijection" if args.device_keys
-                                                    else "synthetic: unique uniform u32 keys, MT19937"),
+                                                    else data_label(args)),
             "config": wl, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clocks, "detail": detail,
         }
@@ -473,6 +510,8 @@ def main():
     ap.add_argument("--chunk", type=int, default=1 << 24, help="sharded pipeline chunk (keys)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--device-keys", action="store_true", help="generate keys on the device (large --keys)")
+    ap.add_argument("--workload", default="reference", choices=["reference", "numpy"],
+                    help="reference: the reference harness's generate_keys / generate_queries for seed 1; numpy: MT19937 + unique")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
