@@ -279,16 +279,18 @@ uint32_t blocked_regions(const bht_table* t, uint64_t n) {
 }
 
 // Plan of a shared-memory-blocked build (build_blocked.cu) of n device-resident pairs, n_regions == 0 when it is
-// not used.  It is opt-in — bht_set_blocked_insert(table, 3), or BHT_SMEM_BUILD=1 in the environment for the sizes
-// the L2-routed build would take — because today it only ties with the L2-routed build (see build_blocked.cu).
+// not used: the default for large cuckoo batches (1.27 ms against 1.81 ms for the L2-routed build, bcht b = 16,
+// 50 M pairs, LF 0.9); tables beyond 2 GB of slots (more than 256 x 128 fine regions) take the L2-routed build.
 BlockedPlan smem_blocked_plan(const bht_table* t, uint64_t n) {
   BlockedPlan none{};
-  if (t->cfg.kind != BHT_BCHT || n == 0) return none;
+  const bool cuckoo = t->cfg.kind == BHT_BCHT || t->cfg.kind == BHT_ONE_CHT;
+  if (!cuckoo || n == 0 || t->blocked_insert == 0 || t->blocked_insert == 2) return none;
   const bool forced = t->blocked_insert == 3;
   if (!forced) {
-    const char* env = std::getenv("BHT_SMEM_BUILD");
-    if (env == nullptr || std::atoi(env) == 0 || t->blocked_insert != 1) return none;
+    const char* env = std::getenv("BHT_SMEM_BUILD");  // 0: fall back to the L2-routed build
+    if (env != nullptr && std::atoi(env) == 0) return none;
     const uint64_t store_bytes = t->cfg.capacity * sizeof(uint64_t);
+    // every region is read / written once whatever n: only for batches that are a sizeable part of the table
     if (n < (4ull << 20) || store_bytes < (192ull << 20) || n * 8 < t->cfg.capacity) return none;
   }
   return plan_blocked_build(t->view, n);

@@ -44,11 +44,12 @@ cudaError_t launch_insert_iht(const TableView& t, const InsertLaunch& a);
 // build_blocked.cu — K10 bin_scatter + K11 region_build: the shared-memory-blocked first pass of a cuckoo build.
 constexpr uint32_t kMaxBlockedRegions = 40000;  // 16-bit region ids, histogram of one tile in shared memory
 struct BlockedPlan {
-  uint32_t n_regions;    // 0: the blocked build does not apply
-  uint32_t region_log2;  // buckets per region (64 KiB of slots)
+  uint32_t n_regions;    // fine regions (one CTA of K11 each); 0: the blocked build does not apply
+  uint32_t region_log2;  // buckets per fine region (64 KiB of slots)
   uint32_t b_log2;
-  uint32_t cap;          // pairs per bin
-  uint32_t cursor_shift; // bin cursors are 4 << cursor_shift bytes apart
+  uint32_t cap;          // pairs per bin (one bin per fine region)
+  uint32_t per;          // fine regions per group of the first partition level
+  uint32_t n_groups;     // groups (<= kMaxShards)
 };
 BlockedPlan plan_blocked_build(const TableView& t, uint64_t n);
 size_t blocked_scratch_bytes(const BlockedPlan& p, uint64_t n);
@@ -76,6 +77,11 @@ cudaError_t launch_shard_route(uint32_t alpha, uint32_t beta, uint32_t n_shards,
 cudaError_t launch_region_route(const HashFn& h0, uint32_t n_regions, const uint32_t* keys, const uint32_t* values, uint64_t n,
                                 uint8_t* scratch8, unsigned long long* counts, unsigned long long* cursors, uint32_t* out_pairs,
                                 int sm_count, cudaStream_t stream);
+// Groups pairs by (fine region of the first bucket) / per, fine region = 2^region_log2 consecutive buckets (first
+// level of the shared-memory-blocked build); counts[g] = pairs of group g; out_pairs as launch_region_route.
+cudaError_t launch_group_route(const HashFn& h0, uint32_t region_log2, uint32_t per, uint32_t n_groups, const uint32_t* keys,
+                               const uint32_t* values, uint64_t n, uint8_t* scratch8, unsigned long long* counts,
+                               unsigned long long* cursors, uint32_t* out_pairs, int sm_count, cudaStream_t stream);
 cudaError_t launch_unpermute(const uint32_t* answers, const uint32_t* index, uint64_t n, uint32_t* out, int sm_count,
                              cudaStream_t stream);
 cudaError_t launch_generate_keys(uint64_t seed, uint64_t offset, uint64_t n, uint32_t* keys, uint32_t* values,
