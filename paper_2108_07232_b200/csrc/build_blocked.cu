@@ -46,7 +46,7 @@ namespace {
 constexpr int kSplitBlock = 256;
 constexpr int kSplitPerThread = 8;
 constexpr int kSplitTile = kSplitBlock * kSplitPerThread;  // 2048 pairs
-constexpr int kBuildBlock = 512;
+constexpr int kBuildBlock = 256;   // few threads with many loads in flight each: 3 CTAs/SM by shared memory
 constexpr uint32_t kStashPairs = 1024;  // per-CTA stash of spilled pairs (K11)
 constexpr uint32_t kRegionBytesLog2 = 16;
 
@@ -192,7 +192,7 @@ region_build_kernel(const __grid_constant__ TableView t, uint32_t region_log2, u
   unsigned long long* rows = reinterpret_cast<unsigned long long*>(sm_bytes);  // region_buckets * B slots
   uint32_t* cnt = reinterpret_cast<uint32_t*>(sm_bytes + (static_cast<size_t>(region_buckets) << (b_log2 + 3)));
   uint2* stash = reinterpret_cast<uint2*>(cnt + region_buckets);
-  __shared__ uint32_t stash_count;
+  __shared__ uint32_t stash_count, placed_count;
   __shared__ unsigned long long stash_base;
   const int lane = threadIdx.x & 31;
   const uint32_t region = blockIdx.x;
@@ -215,7 +215,7 @@ region_build_kernel(const __grid_constant__ TableView t, uint32_t region_log2, u
       if ((n_slots & 1u) && threadIdx.x == 0) rows[n_slots - 1] = gstore[n_slots - 1];
     }
     for (uint32_t i = threadIdx.x; i < nb; i += kBuildBlock) cnt[i] = 0;
-    if (threadIdx.x == 0) stash_count = 0;
+    if (threadIdx.x == 0) stash_count = placed_count = 0;
   }
   __syncthreads();
   if (!fresh) {
@@ -232,7 +232,7 @@ region_build_kernel(const __grid_constant__ TableView t, uint32_t region_log2, u
   const uint32_t n_r = min(bin_cursor[region], cap);
   const uint2* bin = bins + static_cast<uint64_t>(region) * cap;
   uint32_t n_ins = 0;
-  constexpr int U = 4;
+  constexpr int U = 16;  // pairs in flight per thread: a 64 KiB region holds ~29 pairs per thread at load factor 0.9
   for (uint32_t i0 = threadIdx.x; i0 - lane < n_r; i0 += kBuildBlock * U) {  // warp-uniform trip count
     uint2 kv[U];
     bool in[U];
@@ -270,6 +270,12 @@ region_build_kernel(const __grid_constant__ TableView t, uint32_t region_log2, u
       }
     }
   }
+  {  // one set of global counter updates per CTA (not per warp: thousands of CTAs would hammer three addresses)
+    uint32_t w = n_ins;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(kFullMask, w, o);
+    if (lane == 0 && w != 0) atomicAdd(&placed_count, w);
+  }
   __syncthreads();
 
   // phase 2: the region back to the store, coalesced; the stash to the spill list with one global atomic
@@ -283,8 +289,13 @@ region_build_kernel(const __grid_constant__ TableView t, uint32_t region_log2, u
     if (threadIdx.x == 0 && stashed != 0) stash_base = atomicAdd(spill_cursor, static_cast<unsigned long long>(stashed));
     __syncthreads();
     for (uint32_t i = threadIdx.x; i < stashed; i += kBuildBlock) spill[stash_base + i] = stash[i];
+    if (threadIdx.x == 0 && placed_count != 0) {
+      const unsigned long long a = placed_count;
+      atomicAdd(&ctr->inserted, a);
+      atomicAdd(&ctr->inserted_total, a);
+      atomicAdd(&ctr->insert_probes, a);
+    }
   }
-  flush_insert_counters(ctr, lane, n_ins, 0u, n_ins);
 }
 
 }  // namespace
@@ -295,7 +306,10 @@ BlockedPlan plan_blocked_build(const TableView& t, uint64_t n) {
   uint32_t b_log2 = 0;
   while ((1u << b_log2) < t.bucket_size) ++b_log2;
   if (b_log2 > 6 || n == 0 || n > 0xFFFFFFFFull) return p;
-  const uint32_t region_log2 = kRegionBytesLog2 - 3 - b_log2;  // 64 KiB of slots per fine region
+  uint32_t region_bytes_log2 = kRegionBytesLog2;  // 64 KiB of slots per fine region
+  if (const char* e = std::getenv("BHT_REGION_BYTES_LOG2")) region_bytes_log2 = static_cast<uint32_t>(std::atoi(e));  // tuning knob
+  if (region_bytes_log2 < 12 || region_bytes_log2 > 17 || region_bytes_log2 < 3 + b_log2 + 5) return p;
+  const uint32_t region_log2 = region_bytes_log2 - 3 - b_log2;
   const uint64_t regions = (t.num_buckets + (1ull << region_log2) - 1) >> region_log2;
   if (regions > 128ull * kMaxShards) return p;  // two partition levels of <= 256 x 128
   uint32_t per = static_cast<uint32_t>(std::ceil(std::sqrt(static_cast<double>(regions))));
