@@ -18,10 +18,12 @@
 //                       pattern when the table is known to be empty, else loaded from the store), every pair of the
 //                       bin claims slot = atomicAdd(load counter of its bucket) — a shared-memory atomic, no CAS, no
 //                       lost races, no re-probes — and the region is written back with coalesced 16-byte stores.
-//                       A pair whose bucket is full goes to a per-CTA stash that is appended to the global spill
-//                       list once per CTA.
-//   K4  (existing)      the general cuckoo kernel (insert_cuckoo.cu) inserts the spill list: it probes H0, finds
-//                       the bucket full, exchanges a random victim and walks the chain exactly as the reference.
+//                       A pair whose bucket is full goes to a per-CTA stash; once every claim is written the stashed
+//                       pairs do their first eviction in shared memory (atomicExch into a random slot of the full
+//                       bucket, table.cpp:67-81) and the VICTIMS go to the global spill list, each with the bucket
+//                       its walk goes on in and a chain length of 1 (one list reservation per CTA).
+//   K4  (existing)      the general cuckoo kernel (insert_cuckoo.cu) finishes the walks of the spill list exactly as
+//                       the reference would: probe the next bucket, claim or evict again, up to max_chain.
 //
 // What the earlier versions of this file measured on B200 (bcht b = 16, 50 M pairs, LF 0.9; profiles/r01e_*):
 //   * one-level binning with one L2 atomicAdd + one scattered 8-byte store per pair: 1.12 ms — the L2 serves
@@ -32,7 +34,8 @@
 //     (tools/microbench/warp_rank.cu), against 20-34 for ballot ranking and 42-64 for match.any.
 //
 // Probe accounting (probe_stats.hpp:12-31: one probe per bucket inspection): a pair placed by K11 costs one probe;
-// a spilled pair is not counted here — its inspection of the full H0 bucket is the first probe K4 counts for it.
+// a pair that evicts in K11 costs one probe there (the inspection that found its bucket full); K4 counts the rest
+// of the walk.  A pair that overflows a bin or the stash reaches K4 untouched and is counted there from H0 on.
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
@@ -50,16 +53,28 @@ constexpr int kBuildBlock = 256;   // few threads with many loads in flight each
 constexpr uint32_t kStashPairs = 1024;  // per-CTA stash of spilled pairs (K11)
 constexpr uint32_t kRegionBytesLog2 = 16;
 
-// Appends the pairs of the lanes with `spilled` to the global spill list: one global atomic per warp (rare paths).
-__device__ __forceinline__ void spill_append(bool spilled, uint2 kv, uint2* __restrict__ spill,
-                                             unsigned long long* __restrict__ spill_cursor, int lane) {
+// The spill list: packed pairs + where their walk starts (kStartAtH0 for a pair that has not probed anything yet).
+struct Spill {
+  uint2* pairs;
+  uint32_t* start;
+  unsigned long long* cursor;
+};
+
+// Appends the pairs of the lanes with `spilled` to the spill list as fresh pairs: one global atomic per warp (rare paths).
+__device__ __forceinline__ void spill_append(bool spilled, uint2 kv, const Spill& sp, int lane) {
+  uint2* __restrict__ spill = sp.pairs;
+  unsigned long long* __restrict__ spill_cursor = sp.cursor;
   const uint32_t m = __ballot_sync(kFullMask, spilled);
   if (m == 0) return;
   const int leader = __ffs(m) - 1;
   unsigned long long base = 0;
   if (lane == leader) base = atomicAdd(spill_cursor, static_cast<unsigned long long>(__popc(m)));
   base = __shfl_sync(kFullMask, base, leader);
-  if (spilled) spill[base + __popc(m & ((1u << lane) - 1u))] = kv;
+  if (spilled) {
+    const unsigned long long pos = base + __popc(m & ((1u << lane) - 1u));
+    spill[pos] = kv;
+    sp.start[pos] = kStartAtH0;
+  }
 }
 
 // ---- K10 ------------------------------------------------------------------------------------------------------
@@ -68,8 +83,7 @@ __device__ __forceinline__ void spill_append(bool spilled, uint2 kv, uint2* __re
 __global__ void __launch_bounds__(kSplitBlock)
 bin_split_kernel(const __grid_constant__ HashFn h0, uint32_t region_log2, uint32_t per, uint32_t n_groups, uint32_t n_regions,
                  uint32_t cap, const uint2* __restrict__ pairs, uint64_t n, const unsigned long long* __restrict__ group_counts,
-                 uint32_t* __restrict__ bin_cursor, uint2* __restrict__ bins, uint2* __restrict__ spill,
-                 unsigned long long* __restrict__ spill_cursor) {
+                 uint32_t* __restrict__ bin_cursor, uint2* __restrict__ bins, const Spill sp) {
   __shared__ uint2 s_pair[kSplitTile];
   __shared__ uint8_t s_local[kSplitTile];
   __shared__ uint32_t hist[256], tile_off[256], base_of[256], warp_tot[kSplitBlock / 32];
@@ -158,7 +172,7 @@ bin_split_kernel(const __grid_constant__ HashFn h0, uint32_t region_log2, uint32
         s_pair[slot] = kv[j];
         s_local[slot] = static_cast<uint8_t>(local[j]);
       }
-      spill_append(in && !ranked, kv[j], spill, spill_cursor, lane);  // full warps: j is unrolled, no lane has left
+      spill_append(in && !ranked, kv[j], sp, lane);  // full warps: j is unrolled, no lane has left
     }
     __syncthreads();
     const uint32_t ranked_total = tile_off[255] + hist[255];
@@ -175,7 +189,7 @@ bin_split_kernel(const __grid_constant__ HashFn h0, uint32_t region_log2, uint32
         fits = pos < cap;
         if (fits) bins[static_cast<uint64_t>(f_base + l) * cap + pos] = out;
       }
-      spill_append(in && !fits, out, spill, spill_cursor, lane);
+      spill_append(in && !fits, out, sp, lane);
     }
     __syncthreads();
   }
@@ -184,15 +198,15 @@ bin_split_kernel(const __grid_constant__ HashFn h0, uint32_t region_log2, uint32
 // ---- K11 ------------------------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(kBuildBlock)
 region_build_kernel(const __grid_constant__ TableView t, uint32_t region_log2, uint32_t b_log2, uint32_t cap,
-                    const uint32_t* __restrict__ bin_cursor, const uint2* __restrict__ bins, int fresh,
-                    uint2* __restrict__ spill, unsigned long long* __restrict__ spill_cursor, DevCounters* __restrict__ ctr) {
+                    const uint32_t* __restrict__ bin_cursor, const uint2* __restrict__ bins, int fresh, const Spill sp,
+                    DevCounters* __restrict__ ctr) {
   extern __shared__ __align__(16) unsigned char sm_bytes[];
   const uint32_t region_buckets = 1u << region_log2;
   const uint32_t B = 1u << b_log2;
   unsigned long long* rows = reinterpret_cast<unsigned long long*>(sm_bytes);  // region_buckets * B slots
   uint32_t* cnt = reinterpret_cast<uint32_t*>(sm_bytes + (static_cast<size_t>(region_buckets) << (b_log2 + 3)));
   uint2* stash = reinterpret_cast<uint2*>(cnt + region_buckets);
-  __shared__ uint32_t stash_count, placed_count;
+  __shared__ uint32_t stash_count, placed_count, hole_count;
   __shared__ unsigned long long stash_base;
   const int lane = threadIdx.x & 31;
   const uint32_t region = blockIdx.x;
@@ -215,7 +229,7 @@ region_build_kernel(const __grid_constant__ TableView t, uint32_t region_log2, u
       if ((n_slots & 1u) && threadIdx.x == 0) rows[n_slots - 1] = gstore[n_slots - 1];
     }
     for (uint32_t i = threadIdx.x; i < nb; i += kBuildBlock) cnt[i] = 0;
-    if (threadIdx.x == 0) stash_count = placed_count = 0;
+    if (threadIdx.x == 0) stash_count = placed_count = hole_count = 0;
   }
   __syncthreads();
   if (!fresh) {
@@ -266,7 +280,7 @@ region_build_kernel(const __grid_constant__ TableView t, uint32_t region_log2, u
         const uint32_t pos = base + __popc(m & ((1u << lane) - 1u));
         const bool stashed = spilled && pos < kStashPairs;
         if (stashed) stash[pos] = kv[u];
-        spill_append(spilled && !stashed, kv[u], spill, spill_cursor, lane);
+        spill_append(spilled && !stashed, kv[u], sp, lane);
       }
     }
   }
@@ -276,24 +290,54 @@ region_build_kernel(const __grid_constant__ TableView t, uint32_t region_log2, u
     for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(kFullMask, w, o);
     if (lane == 0 && w != 0) atomicAdd(&placed_count, w);
   }
+  __syncthreads();  // every claimed slot is written
+
+  // phase 1b: the first eviction of the stashed pairs, in shared memory (table.cpp:67-81): the pair goes into a random
+  // slot of its full bucket, the victim goes to the spill list with the bucket named by the hash function after the
+  // lowest-index one that maps it here, and a chain length of 1.  One probe (the inspection that found the bucket full).
+  const uint32_t stashed = min(stash_count, kStashPairs);
+  if (threadIdx.x == 0 && stashed != 0) stash_base = atomicAdd(sp.cursor, static_cast<unsigned long long>(stashed));
+  __syncthreads();
+  if (stashed != 0) {
+    uint64_t rng = xorshift_init(mix_seed(t.seed, 0x626C6B64ull + static_cast<uint64_t>(blockIdx.x) * kBuildBlock + threadIdx.x));
+    for (uint32_t i = threadIdx.x; i < stashed; i += kBuildBlock) {
+      const uint2 p = stash[i];
+      const uint32_t bid = bucket_index(t.h[0], p.x);
+      const uint32_t lb = bid - static_cast<uint32_t>(first);
+      const unsigned long long old = atomicExch(rows + (lb << b_log2) + xorshift_next_below(rng, B), pack_pair(p.x, p.y));
+      const uint32_t vk = static_cast<uint32_t>(old);
+      uint32_t next = 0;
+      if (vk != kEmptyKey) {
+        uint32_t cand[4];
+#pragma unroll
+        for (int h = 0; h < 4; ++h) cand[h] = h < static_cast<int>(t.n_hashes) ? bucket_index(t.h[h], vk) : 0u;
+        next = cand[0];
+#pragma unroll
+        for (int h = 3; h >= 0; --h)  // lowest matching index wins (table.cpp:74-80)
+          if (h < static_cast<int>(t.n_hashes) && cand[h] == bid) next = cand[h + 1 < static_cast<int>(t.n_hashes) ? h + 1 : 0];
+      }
+      // a hole (only on an uploaded store): the pair is simply placed; the reserved list entry becomes a tombstone
+      if (vk == kEmptyKey) atomicAdd(&hole_count, 1u);
+      sp.pairs[stash_base + i] = make_uint2(vk, static_cast<uint32_t>(old >> 32));
+      sp.start[stash_base + i] = next | 0x80000000u;
+    }
+  }
   __syncthreads();
 
-  // phase 2: the region back to the store, coalesced; the stash to the spill list with one global atomic
+  // phase 2: the region back to the store, coalesced
   {
     const uint4* rows4 = reinterpret_cast<const uint4*>(rows);
     uint4* g4 = reinterpret_cast<uint4*>(gstore);
     const uint32_t n4 = n_slots >> 1;
     for (uint32_t i = threadIdx.x; i < n4; i += kBuildBlock) g4[i] = rows4[i];
     if ((n_slots & 1u) && threadIdx.x == 0) gstore[n_slots - 1] = rows[n_slots - 1];
-    const uint32_t stashed = min(stash_count, kStashPairs);
-    if (threadIdx.x == 0 && stashed != 0) stash_base = atomicAdd(spill_cursor, static_cast<unsigned long long>(stashed));
-    __syncthreads();
-    for (uint32_t i = threadIdx.x; i < stashed; i += kBuildBlock) spill[stash_base + i] = stash[i];
-    if (threadIdx.x == 0 && placed_count != 0) {
-      const unsigned long long a = placed_count;
-      atomicAdd(&ctr->inserted, a);
-      atomicAdd(&ctr->inserted_total, a);
-      atomicAdd(&ctr->insert_probes, a);
+    if (threadIdx.x == 0 && (placed_count != 0 || stashed != 0)) {
+      const unsigned long long a = static_cast<unsigned long long>(placed_count) + hole_count;
+      if (a != 0) {
+        atomicAdd(&ctr->inserted, a);
+        atomicAdd(&ctr->inserted_total, a);
+      }
+      atomicAdd(&ctr->insert_probes, static_cast<unsigned long long>(placed_count) + stashed);
     }
   }
 }
@@ -311,7 +355,7 @@ BlockedPlan plan_blocked_build(const TableView& t, uint64_t n) {
   if (region_bytes_log2 < 12 || region_bytes_log2 > 17 || region_bytes_log2 < 3 + b_log2 + 5) return p;
   const uint32_t region_log2 = region_bytes_log2 - 3 - b_log2;
   const uint64_t regions = (t.num_buckets + (1ull << region_log2) - 1) >> region_log2;
-  if (regions > 128ull * kMaxShards) return p;  // two partition levels of <= 256 x 128
+  if (regions > 128ull * kMaxShards || t.num_buckets > 0x7FFFFFFFull) return p;  // two levels of <= 256 x 128; 31-bit start buckets
   uint32_t per = static_cast<uint32_t>(std::ceil(std::sqrt(static_cast<double>(regions))));
   if (per < 1) per = 1;
   if (per > 128) per = 128;
@@ -330,15 +374,15 @@ BlockedPlan plan_blocked_build(const TableView& t, uint64_t n) {
 }
 
 // scratch layout: grouped pairs (n) | bins (n_regions * cap) | spill (n) | spill_cursor (8) pad (8) | bin_cursor (n_regions)
-//                 | group counts + cursors (2 * n_groups u64) | destination bytes of the group route (n)
+//                 | group counts + cursors (2 * n_groups u64) | spill start words (n) | destination bytes of the group route (n)
 size_t blocked_scratch_bytes(const BlockedPlan& p, uint64_t n) {
   return n * 8 + static_cast<size_t>(p.n_regions) * p.cap * 8 + n * 8 + 16 + static_cast<size_t>(p.n_regions) * 4 + 16 +
-         2 * static_cast<size_t>(p.n_groups) * 8 + n + 64;
+         2 * static_cast<size_t>(p.n_groups) * 8 + n * 4 + n + 64;
 }
 
 cudaError_t launch_blocked_build(const TableView& t, const BlockedPlan& p, const uint32_t* keys, const uint32_t* values,
                                  uint64_t n, bool fresh, void* scratch, DevCounters* ctr, int sm_count, cudaStream_t stream,
-                                 const uint2** spill_out, const unsigned long long** spill_count_out) {
+                                 PairSource* spill_out, const unsigned long long** spill_count_out) {
   unsigned char* s = static_cast<unsigned char*>(scratch);
   uint2* grouped = reinterpret_cast<uint2*>(s);
   uint2* bins = grouped + n;
@@ -348,7 +392,9 @@ cudaError_t launch_blocked_build(const TableView& t, const BlockedPlan& p, const
   unsigned long long* group_counts = reinterpret_cast<unsigned long long*>(
       (reinterpret_cast<uintptr_t>(bin_cursor + p.n_regions) + 15) & ~static_cast<uintptr_t>(15));
   unsigned long long* group_cursors = group_counts + p.n_groups;
-  uint8_t* dest8 = reinterpret_cast<uint8_t*>(group_cursors + p.n_groups);
+  uint32_t* spill_start = reinterpret_cast<uint32_t*>(group_cursors + p.n_groups);
+  uint8_t* dest8 = reinterpret_cast<uint8_t*>(spill_start + n);
+  const Spill sp{spill, spill_start, spill_cursor};
   cudaError_t e = cudaMemsetAsync(spill_cursor, 0, 16 + static_cast<size_t>(p.n_regions) * 4, stream);
   if (e != cudaSuccess) return e;
 
@@ -359,7 +405,7 @@ cudaError_t launch_blocked_build(const TableView& t, const BlockedPlan& p, const
   const uint64_t tiles = (n + kSplitTile - 1) / kSplitTile;
   const int grid_b = static_cast<int>(std::min<uint64_t>(tiles, static_cast<uint64_t>(sm_count) * 8));
   bin_split_kernel<<<grid_b, kSplitBlock, 0, stream>>>(t.h[0], p.region_log2, p.per, p.n_groups, p.n_regions, p.cap, grouped, n,
-                                                      group_counts, bin_cursor, bins, spill, spill_cursor);
+                                                      group_counts, bin_cursor, bins, sp);
   note_launch();
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
@@ -368,9 +414,11 @@ cudaError_t launch_blocked_build(const TableView& t, const BlockedPlan& p, const
   e = cudaFuncSetAttribute(region_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_c);
   if (e != cudaSuccess) return e;
   region_build_kernel<<<p.n_regions, kBuildBlock, smem_c, stream>>>(t, p.region_log2, p.b_log2, p.cap, bin_cursor, bins,
-                                                                   fresh ? 1 : 0, spill, spill_cursor, ctr);
+                                                                   fresh ? 1 : 0, sp, ctr);
   note_launch();
-  *spill_out = spill;
+  spill_out->keys = reinterpret_cast<const uint32_t*>(spill);
+  spill_out->values = nullptr;
+  spill_out->start = spill_start;
   *spill_count_out = spill_cursor;
   return cudaGetLastError();
 }

@@ -368,13 +368,13 @@ bht_status do_insert(bht_table* t, const uint32_t* keys, const uint32_t* values,
       // first bucket was full (their count stays on the device).
       void* scratch = nullptr;
       BHT_CUDA(cudaMallocAsync(&scratch, blocked_scratch_bytes(plan, n), stream));
-      const uint2* spill = nullptr;
+      PairSource spill{};
       const unsigned long long* spill_count = nullptr;
       cudaError_t e = launch_blocked_build(t->view, plan, keys, values, n, t->known_empty, scratch, t->ctr, t->sm_count, stream,
                                            &spill, &spill_count);
       if (e == cudaSuccess) e = cudaEventRecord(t->phase_ev[1], stream);
       if (e == cudaSuccess)
-        e = launch_insert_kind(t, PairSource{reinterpret_cast<const uint32_t*>(spill), nullptr}, n, 0, stream, false, spill_count);
+        e = launch_insert_kind(t, spill, n, 0, stream, false, spill_count);
       cudaFreeAsync(scratch, stream);
       if (e != cudaSuccess) return cuda_fail(e, "bht_insert (shared-memory blocked)");
     } else if (regions > 1) {

@@ -29,7 +29,7 @@ __device__ __forceinline__ void flush_insert_counters(DevCounters* ctr, int lane
 // round ahead; idle lanes take them in order.
 struct PairFeed {
   Stream st;
-  uint32_t ahead_k, ahead_v;
+  uint32_t ahead_k, ahead_v, ahead_s;
   uint32_t ahead_n;  // how many of the 32 prefetched pairs exist (warp-uniform)
 
   // src / shift / cursor are kernel parameters: passed at every call rather than kept in registers
@@ -41,6 +41,8 @@ struct PairFeed {
     uint64_t g;
     const bool in = st.index(lane, shift, g);
     ahead_k = ahead_v = 0u;
+    ahead_s = kStartAtH0;
+    if (in && src.start != nullptr) ahead_s = __ldcs(src.start + g);  // kernel-uniform pointer test
     if (in) {
       if (src.values == nullptr) {  // kernel-uniform
         const uint2 kv = __ldcs(reinterpret_cast<const uint2*>(src.keys) + g);
@@ -55,16 +57,19 @@ struct PairFeed {
   }
   // Returns true for lanes that received a fresh pair.
   __device__ __forceinline__ bool refill(const PairSource& src, uint32_t shift, uint32_t* cursor, bool have, int lane,
-                                         uint32_t& key, uint32_t& val) {
+                                         uint32_t& key, uint32_t& val, uint32_t* start = nullptr) {
     const uint32_t idle = __ballot_sync(kFullMask, !have);
     if (idle == 0 || ahead_n == 0) return false;
     const uint32_t rank = __popc(idle & ((1u << lane) - 1u));
     const uint32_t fk = __shfl_sync(kFullMask, ahead_k, rank);
     const uint32_t fv = __shfl_sync(kFullMask, ahead_v, rank);
+    uint32_t fs = kStartAtH0;
+    if (start != nullptr && src.start != nullptr) fs = __shfl_sync(kFullMask, ahead_s, rank);  // warp-uniform branch
     const bool got = !have && rank < ahead_n;
     if (got) {
       key = fk;
       val = fv;
+      if (start != nullptr) *start = fs;
     }
     st.advance(min(static_cast<uint32_t>(__popc(idle)), ahead_n), shift, cursor, lane);
     prefetch(src, shift, lane);

@@ -68,10 +68,14 @@ bulk_insert_cuckoo_kernel(const __grid_constant__ TableView t, const PairSource 
   }
 
   for (;;) {
-    if (feed.refill(src, t.chunk_log2, work_cursor, have, lane, key, val)) {
+    uint32_t start = kStartAtH0;
+    if (feed.refill(src, t.chunk_log2, work_cursor, have, lane, key, val, &start)) {
       have = true;
-      bid = bucket_index(t.h[0], key);
-      chain = 0;
+      // a fresh pair starts at H0 with an empty chain; a victim of the blocked build's in-place first eviction goes
+      // on where build_blocked.cu left it
+      bid = start == kStartAtH0 ? bucket_index(t.h[0], key) : (start & 0x7FFFFFFFu);
+      chain = start == kStartAtH0 ? 0u : (start >> 31);
+      if (src.start != nullptr && key == kEmptyKey) have = false;  // tombstone of the blocked build (a hole was filled)
       retries = 0;
       hint = kNoHint;
     }

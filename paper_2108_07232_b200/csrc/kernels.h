@@ -18,7 +18,11 @@ cudaError_t launch_find(const TableView& t, bool early_exit, const uint32_t* key
 struct PairSource {
   const uint32_t* keys;
   const uint32_t* values;  // null: `keys` holds packed pairs
+  // cuckoo kernel only, optional: where the walk of pair i starts — bits 0..30 the bucket, bit 31 the chain length
+  // so far (0 or 1) — for pairs whose first eviction already happened (build_blocked.cu); kStartAtH0 = a fresh pair
+  const uint32_t* start = nullptr;
 };
+constexpr uint32_t kStartAtH0 = 0xFFFFFFFFu;
 
 struct InsertLaunch {
   PairSource src;
@@ -53,11 +57,12 @@ struct BlockedPlan {
 };
 BlockedPlan plan_blocked_build(const TableView& t, uint64_t n);
 size_t blocked_scratch_bytes(const BlockedPlan& p, uint64_t n);
-// Places every pair whose H0 bucket has room; the others are left in *spill_out (packed pairs, *spill_count_out of
-// them, both device pointers into `scratch`) for launch_insert_cuckoo.
+// Places every pair whose H0 bucket has room; for the others the first eviction is done in place and the victim is
+// left in *spill_out (packed pairs + where their walk goes on, *spill_count_out of them, device pointers into
+// `scratch`) for launch_insert_cuckoo.
 cudaError_t launch_blocked_build(const TableView& t, const BlockedPlan& p, const uint32_t* keys, const uint32_t* values,
                                  uint64_t n, bool fresh, void* scratch, DevCounters* ctr, int sm_count, cudaStream_t stream,
-                                 const uint2** spill_out, const unsigned long long** spill_count_out);
+                                 PairSource* spill_out, const unsigned long long** spill_count_out);
 
 // util.cu — K0 fill, K7 count, admissibility, hash hook, K8/K9 shard routing, synthetic keys.
 cudaError_t launch_fill_empty(uint64_t* store, uint64_t n_slots, int sm_count, cudaStream_t stream);
