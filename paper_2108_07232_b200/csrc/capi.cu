@@ -287,6 +287,10 @@ BlockedPlan smem_blocked_plan(const bht_table* t, uint64_t n) {
   if (!cuckoo || n == 0 || t->blocked_insert == 0 || t->blocked_insert == 2) return none;
   const bool forced = t->blocked_insert == 3;
   if (!forced) {
+    // 1cht takes the L2-routed build by default: the blocked build makes every first attempt before any eviction walk,
+    // which at b = 1 shifts the probe means 1.6-3 % below the reference's interleaved process (2.0225 against 2.0554
+    // probes per insert at LF 0.8) for a 4-9 % gain in time; at b = 16 the shift is 0.1 % and the gain 50 %.
+    if (t->cfg.kind != BHT_BCHT) return none;
     const char* env = std::getenv("BHT_SMEM_BUILD");  // 0: fall back to the L2-routed build
     if (env != nullptr && std::atoi(env) == 0) return none;
     const uint64_t store_bytes = t->cfg.capacity * sizeof(uint64_t);
