@@ -5,11 +5,12 @@
 // — but the first attempt of every pair, which is ~90 % of all the probes of a build at load factor 0.9, never
 // touches HBM at random and never issues a global compare-and-swap:
 //
-//   K8g group route     (util.cu, the router of the L2-blocked build) groups the pairs by GROUP = `per` consecutive
+//   K8g group_scatter   first partition level, one streaming pass: the pairs are grouped by GROUP = `per` consecutive
 //                       fine regions; a fine region is 64 KiB of consecutive buckets (512 buckets at b = 16), a
-//                       444 MB table has 6782 of them in 83 groups of 82.
-//   K10 bin_split       second partition level: tiles of 2048 grouped pairs are ranked by fine region in shared
-//                       memory (a tile spans at most two groups: <= 2 * per <= 256 destinations), one global
+//                       444 MB table has 6782 of them in 83 groups of 82.  Fixed-capacity group segments (the hash is
+//                       uniform): no histogram pre-pass.
+//   K10 bin_split       second partition level: tiles of 2048 pairs of one group are ranked by fine region in shared
+//                       memory (<= per <= 256 destinations), one global
 //                       atomicAdd per (tile, region) reserves a run in the region's bin, and the tile is written out
 //                       run by run (~25 pairs = 200 contiguous bytes per run: whole 32-byte sectors, which is what
 //                       the L2 wants — see the measurements below).  Bins have a fixed capacity (mean + 6 sigma of a
@@ -77,71 +78,140 @@ __device__ __forceinline__ void spill_append(bool spilled, uint2 kv, const Spill
   }
 }
 
-// ---- K10 ------------------------------------------------------------------------------------------------------
-// pairs: n packed pairs grouped by group (group g = fine regions [g * per, (g + 1) * per)); group_counts[g] = pairs
-// of group g.  bins[f * cap ..] / bin_cursor[f]: the bin of fine region f.
+// ---- K8g ------------------------------------------------------------------------------------------------------
+// First partition level, one pass: every pair goes to the segment of its GROUP (= `per` consecutive fine regions).
+// Tiles of 2048 pairs are ranked by group in shared memory, one global atomicAdd per (tile, group) reserves a run in
+// the group's fixed-capacity segment, the tile is staged by group and written out run by run (~25 pairs per run).
+// No histogram pre-pass and no destination bytes: the hash is uniform, so the segments are sized mean + 6 sigma and the
+// few pairs that do not fit go to the spill list.
+__device__ __forceinline__ uint4 load_group4(const uint32_t* __restrict__ p, uint64_t i, uint64_t n, bool aligned) {
+  if (aligned && i + 4 <= n) return __ldcs(reinterpret_cast<const uint4*>(p + i));
+  uint4 r = make_uint4(0, 0, 0, 0);
+  if (i < n) r.x = p[i];
+  if (i + 1 < n) r.y = p[i + 1];
+  if (i + 2 < n) r.z = p[i + 2];
+  if (i + 3 < n) r.w = p[i + 3];
+  return r;
+}
+
 __global__ void __launch_bounds__(kSplitBlock)
-bin_split_kernel(const __grid_constant__ HashFn h0, uint32_t region_log2, uint32_t per, uint32_t n_groups, uint32_t n_regions,
-                 uint32_t cap, const uint2* __restrict__ pairs, uint64_t n, const unsigned long long* __restrict__ group_counts,
-                 uint32_t* __restrict__ bin_cursor, uint2* __restrict__ bins, const Spill sp) {
+group_scatter_kernel(const __grid_constant__ HashFn h0, uint32_t region_log2, uint32_t inv_per, uint32_t n_groups, uint32_t group_cap,
+                     const uint32_t* __restrict__ keys, const uint32_t* __restrict__ values, uint64_t n, bool aligned,
+                     uint32_t* __restrict__ group_cursor, uint2* __restrict__ grouped, const Spill sp) {
   __shared__ uint2 s_pair[kSplitTile];
-  __shared__ uint8_t s_local[kSplitTile];
+  __shared__ uint8_t s_dest[kSplitTile];
   __shared__ uint32_t hist[256], tile_off[256], base_of[256], warp_tot[kSplitBlock / 32];
-  __shared__ unsigned long long group_end[kMaxShards];  // inclusive prefix sums of group_counts
-  __shared__ unsigned long long wsum[kSplitBlock / 32];
-  __shared__ uint32_t s_first_group;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-
-  // prefix sums of the group sizes (n_groups <= 256 = one per thread)
-  {
-    const unsigned long long c = threadIdx.x < n_groups ? group_counts[threadIdx.x] : 0ull;
-    unsigned long long x = c;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const unsigned long long y = __shfl_up_sync(kFullMask, x, o);
-      if (lane >= o) x += y;
-    }
-    if (lane == 31) wsum[warp] = x;
-    __syncthreads();
-    unsigned long long before = 0;
-    for (int w = 0; w < warp; ++w) before += wsum[w];
-    group_end[threadIdx.x] = before + x;
-    __syncthreads();
-  }
-
   const uint64_t n_tiles = (n + kSplitTile - 1) / kSplitTile;
   for (uint64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
     const uint64_t i0 = tile * kSplitTile;
     hist[threadIdx.x] = 0;
-    // group of the tile's first pair = number of groups that end at or before i0
+    __syncthreads();
+    uint32_t k[2][4], v[2][4], dst[2][4], rank[2][4];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const uint64_t i = i0 + (static_cast<uint64_t>(j) * kSplitBlock + threadIdx.x) * 4;
+      const uint4 k4 = load_group4(keys, i, n, aligned), v4 = load_group4(values, i, n, aligned);
+      k[j][0] = k4.x, k[j][1] = k4.y, k[j][2] = k4.z, k[j][3] = k4.w;
+      v[j][0] = v4.x, v[j][1] = v4.y, v[j][2] = v4.z, v[j][3] = v4.w;
+    }
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const uint64_t i = i0 + (static_cast<uint64_t>(j) * kSplitBlock + threadIdx.x) * 4;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        dst[j][e] = static_cast<uint32_t>((static_cast<uint64_t>(bucket_index(h0, k[j][e]) >> region_log2) * inv_per) >> 32);
+        rank[j][e] = 0;
+        if (i + e < n) rank[j][e] = atomicAdd(&hist[dst[j][e]], 1u);
+      }
+    }
+    __syncthreads();
     {
-      const bool ends_before = threadIdx.x < n_groups && group_end[threadIdx.x] <= i0;
-      const uint32_t cnt = __popc(__ballot_sync(kFullMask, ends_before));
-      if (lane == 0) warp_tot[warp] = cnt;
+      const uint32_t h = hist[threadIdx.x];
+      uint32_t x = h;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFullMask, x, o);
+        if (lane >= o) x += y;
+      }
+      if (lane == 31) warp_tot[warp] = x;
+      __syncthreads();
+      uint32_t before = 0;
+      for (int w = 0; w < warp; ++w) before += warp_tot[w];
+      tile_off[threadIdx.x] = before + x - h;
+      base_of[threadIdx.x] = (h != 0 && threadIdx.x < n_groups) ? atomicAdd(&group_cursor[threadIdx.x], h) : 0u;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-      uint32_t g = 0;
-      for (int w = 0; w < kSplitBlock / 32; ++w) g += warp_tot[w];
-      s_first_group = g;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const uint64_t i = i0 + (static_cast<uint64_t>(j) * kSplitBlock + threadIdx.x) * 4;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        if (i + e < n) {
+          const uint32_t slot = tile_off[dst[j][e]] + rank[j][e];
+          s_pair[slot] = make_uint2(k[j][e], v[j][e]);
+          s_dest[slot] = static_cast<uint8_t>(dst[j][e]);
+        }
+      }
     }
     __syncthreads();
-    const uint32_t f_base = s_first_group * per;
+    const uint32_t in_tile = static_cast<uint32_t>(n - i0 < kSplitTile ? n - i0 : kSplitTile);
+#pragma unroll
+    for (int j = 0; j < kSplitPerThread; ++j) {
+      const uint32_t slot = j * kSplitBlock + threadIdx.x;
+      const bool in = slot < in_tile;
+      uint2 out = make_uint2(0u, 0u);
+      bool fits = false;
+      if (in) {
+        const uint32_t d = s_dest[slot];
+        const uint32_t pos = base_of[d] + (slot - tile_off[d]);
+        out = s_pair[slot];
+        fits = pos < group_cap;
+        if (fits) __stcs(grouped + static_cast<uint64_t>(d) * group_cap + pos, out);
+      }
+      spill_append(in && !fits, out, sp, lane);
+    }
+    __syncthreads();
+  }
+}
+
+// ---- K10 ------------------------------------------------------------------------------------------------------
+// grouped: segment g = pairs of group g (fine regions [g * per, (g + 1) * per)), group_cursor[g] of them (clamped to
+// group_cap).  bins[f * cap ..] / bin_cursor[f]: the bin of fine region f.  A tile never leaves its group.
+__global__ void __launch_bounds__(kSplitBlock)
+bin_split_kernel(const __grid_constant__ HashFn h0, uint32_t region_log2, uint32_t per, uint32_t n_groups, uint32_t n_regions,
+                 uint32_t cap, uint32_t group_cap, const uint2* __restrict__ grouped, const uint32_t* __restrict__ group_cursor,
+                 uint32_t* __restrict__ bin_cursor, uint2* __restrict__ bins, const Spill sp) {
+  __shared__ uint2 s_pair[kSplitTile];
+  __shared__ uint8_t s_local[kSplitTile];
+  __shared__ uint32_t hist[256], tile_off[256], base_of[256], warp_tot[kSplitBlock / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t tiles_per_group = (group_cap + kSplitTile - 1) / kSplitTile;
+  const uint64_t n_tiles = static_cast<uint64_t>(n_groups) * tiles_per_group;
+  for (uint64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    const uint32_t g = static_cast<uint32_t>(tile / tiles_per_group);
+    const uint32_t t0 = static_cast<uint32_t>(tile % tiles_per_group) * kSplitTile;
+    const uint32_t in_group = min(group_cursor[g], group_cap);
+    if (t0 >= in_group) continue;  // block-uniform
+    const uint32_t len = min(static_cast<uint32_t>(kSplitTile), in_group - t0);
+    const uint2* src = grouped + static_cast<uint64_t>(g) * group_cap + t0;
+    const uint32_t f_base = g * per;
+    hist[threadIdx.x] = 0;
+    __syncthreads();
 
     uint2 kv[kSplitPerThread];
     uint32_t local[kSplitPerThread], rank[kSplitPerThread];
 #pragma unroll
     for (int j = 0; j < kSplitPerThread; ++j) {
-      const uint64_t i = i0 + j * kSplitBlock + threadIdx.x;
-      kv[j] = i < n ? __ldcs(pairs + i) : make_uint2(0u, 0u);
+      const uint32_t i = j * kSplitBlock + threadIdx.x;
+      kv[j] = i < len ? __ldcs(src + i) : make_uint2(0u, 0u);
     }
 #pragma unroll
     for (int j = 0; j < kSplitPerThread; ++j) {
-      const uint64_t i = i0 + j * kSplitBlock + threadIdx.x;
-      const uint32_t f = bucket_index(h0, kv[j].x) >> region_log2;
-      local[j] = f - f_base;  // a tile that spans more than two groups (tiny tables) overflows 255: handled below
+      const uint32_t i = j * kSplitBlock + threadIdx.x;
+      local[j] = (bucket_index(h0, kv[j].x) >> region_log2) - f_base;  // < per <= 256 for every pair of the group
       rank[j] = 0;
-      if (i < n && local[j] < 256u) rank[j] = atomicAdd(&hist[local[j]], 1u);
+      if (i < len && local[j] < 256u) rank[j] = atomicAdd(&hist[local[j]], 1u);
     }
     __syncthreads();
     // exclusive scan of hist + one global reservation per destination of the tile
@@ -164,22 +234,18 @@ bin_split_kernel(const __grid_constant__ HashFn h0, uint32_t region_log2, uint32
     __syncthreads();
 #pragma unroll
     for (int j = 0; j < kSplitPerThread; ++j) {
-      const uint64_t i = i0 + j * kSplitBlock + threadIdx.x;
-      const bool in = i < n;
-      const bool ranked = in && local[j] < 256u;
-      if (ranked) {
+      const uint32_t i = j * kSplitBlock + threadIdx.x;
+      if (i < len && local[j] < 256u) {
         const uint32_t slot = tile_off[local[j]] + rank[j];
         s_pair[slot] = kv[j];
         s_local[slot] = static_cast<uint8_t>(local[j]);
       }
-      spill_append(in && !ranked, kv[j], sp, lane);  // full warps: j is unrolled, no lane has left
     }
     __syncthreads();
-    const uint32_t ranked_total = tile_off[255] + hist[255];
 #pragma unroll
     for (int j = 0; j < kSplitPerThread; ++j) {
       const uint32_t slot = j * kSplitBlock + threadIdx.x;
-      const bool in = slot < ranked_total;
+      const bool in = slot < len;
       uint2 out = make_uint2(0u, 0u);
       bool fits = false;
       if (in) {
@@ -355,10 +421,10 @@ BlockedPlan plan_blocked_build(const TableView& t, uint64_t n) {
   if (region_bytes_log2 < 12 || region_bytes_log2 > 17 || region_bytes_log2 < 3 + b_log2 + 5) return p;
   const uint32_t region_log2 = region_bytes_log2 - 3 - b_log2;
   const uint64_t regions = (t.num_buckets + (1ull << region_log2) - 1) >> region_log2;
-  if (regions > 128ull * kMaxShards || t.num_buckets > 0x7FFFFFFFull) return p;  // two levels of <= 256 x 128; 31-bit start buckets
+  if (regions > 256ull * kMaxShards || t.num_buckets > 0x7FFFFFFFull) return p;  // two levels of <= 256 x 256; 31-bit start buckets
   uint32_t per = static_cast<uint32_t>(std::ceil(std::sqrt(static_cast<double>(regions))));
   if (per < 1) per = 1;
-  if (per > 128) per = 128;
+  if (per > 256) per = 256;
   const uint32_t groups = static_cast<uint32_t>((regions + per - 1) / per);
   if (groups > static_cast<uint32_t>(kMaxShards)) return p;
   const double mean = static_cast<double>(n) * static_cast<double>(1ull << region_log2) / static_cast<double>(t.num_buckets);
@@ -370,14 +436,18 @@ BlockedPlan plan_blocked_build(const TableView& t, uint64_t n) {
   p.b_log2 = b_log2;
   p.per = per;
   p.n_groups = groups;
+  const double gmean = mean * per;
+  double gcap = gmean + 6.0 * std::sqrt(gmean) + 64.0;
+  if (gcap > static_cast<double>(n)) gcap = static_cast<double>(n);
+  p.group_cap = (static_cast<uint32_t>(gcap) + 2u) & ~1u;
   return p;
 }
 
-// scratch layout: grouped pairs (n) | bins (n_regions * cap) | spill (n) | spill_cursor (8) pad (8) | bin_cursor (n_regions)
-//                 | group counts + cursors (2 * n_groups u64) | spill start words (n) | destination bytes of the group route (n)
+// scratch layout: grouped pairs (n_groups * group_cap) | bins (n_regions * cap) | spill pairs (n) | spill_cursor (8) pad (8)
+//                 | bin_cursor (n_regions) | group_cursor (n_groups) | pad to 16 | spill start words (n)
 size_t blocked_scratch_bytes(const BlockedPlan& p, uint64_t n) {
-  return n * 8 + static_cast<size_t>(p.n_regions) * p.cap * 8 + n * 8 + 16 + static_cast<size_t>(p.n_regions) * 4 + 16 +
-         2 * static_cast<size_t>(p.n_groups) * 8 + n * 4 + n + 64;
+  return static_cast<size_t>(p.n_groups) * p.group_cap * 8 + static_cast<size_t>(p.n_regions) * p.cap * 8 + n * 8 + 16 +
+         (static_cast<size_t>(p.n_regions) + p.n_groups) * 4 + 16 + n * 4 + 64;
 }
 
 cudaError_t launch_blocked_build(const TableView& t, const BlockedPlan& p, const uint32_t* keys, const uint32_t* values,
@@ -385,27 +455,31 @@ cudaError_t launch_blocked_build(const TableView& t, const BlockedPlan& p, const
                                  PairSource* spill_out, const unsigned long long** spill_count_out) {
   unsigned char* s = static_cast<unsigned char*>(scratch);
   uint2* grouped = reinterpret_cast<uint2*>(s);
-  uint2* bins = grouped + n;
+  uint2* bins = grouped + static_cast<size_t>(p.n_groups) * p.group_cap;
   uint2* spill = bins + static_cast<size_t>(p.n_regions) * p.cap;
   unsigned long long* spill_cursor = reinterpret_cast<unsigned long long*>(spill + n);
   uint32_t* bin_cursor = reinterpret_cast<uint32_t*>(spill_cursor + 2);
-  unsigned long long* group_counts = reinterpret_cast<unsigned long long*>(
-      (reinterpret_cast<uintptr_t>(bin_cursor + p.n_regions) + 15) & ~static_cast<uintptr_t>(15));
-  unsigned long long* group_cursors = group_counts + p.n_groups;
-  uint32_t* spill_start = reinterpret_cast<uint32_t*>(group_cursors + p.n_groups);
-  uint8_t* dest8 = reinterpret_cast<uint8_t*>(spill_start + n);
+  uint32_t* group_cursor = bin_cursor + p.n_regions;
+  uint32_t* spill_start = reinterpret_cast<uint32_t*>(
+      (reinterpret_cast<uintptr_t>(group_cursor + p.n_groups) + 15) & ~static_cast<uintptr_t>(15));
   const Spill sp{spill, spill_start, spill_cursor};
-  cudaError_t e = cudaMemsetAsync(spill_cursor, 0, 16 + static_cast<size_t>(p.n_regions) * 4, stream);
+  cudaError_t e = cudaMemsetAsync(spill_cursor, 0, 16 + (static_cast<size_t>(p.n_regions) + p.n_groups) * 4, stream);
   if (e != cudaSuccess) return e;
 
-  e = launch_group_route(t.h[0], p.region_log2, p.per, p.n_groups, keys, values, n, dest8, group_counts, group_cursors,
-                         reinterpret_cast<uint32_t*>(grouped), sm_count, stream);
+  const bool aligned = ((reinterpret_cast<uintptr_t>(keys) | reinterpret_cast<uintptr_t>(values)) & 15) == 0;
+  const uint32_t inv_per = static_cast<uint32_t>((1ull << 32) / p.per) + 1u;  // exact quotient for fine ids < 2^16, per <= 256
+  const uint64_t tiles_a = (n + kSplitTile - 1) / kSplitTile;
+  const int grid_a = static_cast<int>(std::min<uint64_t>(tiles_a, static_cast<uint64_t>(sm_count) * 8));
+  group_scatter_kernel<<<grid_a, kSplitBlock, 0, stream>>>(t.h[0], p.region_log2, inv_per, p.n_groups, p.group_cap, keys, values, n,
+                                                          aligned, group_cursor, grouped, sp);
+  note_launch();
+  e = cudaGetLastError();
   if (e != cudaSuccess) return e;
 
-  const uint64_t tiles = (n + kSplitTile - 1) / kSplitTile;
-  const int grid_b = static_cast<int>(std::min<uint64_t>(tiles, static_cast<uint64_t>(sm_count) * 8));
-  bin_split_kernel<<<grid_b, kSplitBlock, 0, stream>>>(t.h[0], p.region_log2, p.per, p.n_groups, p.n_regions, p.cap, grouped, n,
-                                                      group_counts, bin_cursor, bins, sp);
+  const uint64_t tiles_b = static_cast<uint64_t>(p.n_groups) * ((p.group_cap + kSplitTile - 1) / kSplitTile);
+  const int grid_b = static_cast<int>(std::min<uint64_t>(tiles_b, static_cast<uint64_t>(sm_count) * 8));
+  bin_split_kernel<<<grid_b, kSplitBlock, 0, stream>>>(t.h[0], p.region_log2, p.per, p.n_groups, p.n_regions, p.cap, p.group_cap,
+                                                      grouped, group_cursor, bin_cursor, bins, sp);
   note_launch();
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;

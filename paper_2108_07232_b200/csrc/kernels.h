@@ -54,6 +54,7 @@ struct BlockedPlan {
   uint32_t cap;          // pairs per bin (one bin per fine region)
   uint32_t per;          // fine regions per group of the first partition level
   uint32_t n_groups;     // groups (<= kMaxShards)
+  uint32_t group_cap;    // pairs per group segment
 };
 BlockedPlan plan_blocked_build(const TableView& t, uint64_t n);
 size_t blocked_scratch_bytes(const BlockedPlan& p, uint64_t n);
