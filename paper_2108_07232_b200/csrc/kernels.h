@@ -83,11 +83,6 @@ cudaError_t launch_shard_route(uint32_t alpha, uint32_t beta, uint32_t n_shards,
 cudaError_t launch_region_route(const HashFn& h0, uint32_t n_regions, const uint32_t* keys, const uint32_t* values, uint64_t n,
                                 uint8_t* scratch8, unsigned long long* counts, unsigned long long* cursors, uint32_t* out_pairs,
                                 int sm_count, cudaStream_t stream);
-// Groups pairs by (fine region of the first bucket) / per, fine region = 2^region_log2 consecutive buckets (first
-// level of the shared-memory-blocked build); counts[g] = pairs of group g; out_pairs as launch_region_route.
-cudaError_t launch_group_route(const HashFn& h0, uint32_t region_log2, uint32_t per, uint32_t n_groups, const uint32_t* keys,
-                               const uint32_t* values, uint64_t n, uint8_t* scratch8, unsigned long long* counts,
-                               unsigned long long* cursors, uint32_t* out_pairs, int sm_count, cudaStream_t stream);
 cudaError_t launch_unpermute(const uint32_t* answers, const uint32_t* index, uint64_t n, uint32_t* out, int sm_count,
                              cudaStream_t stream);
 cudaError_t launch_generate_keys(uint64_t seed, uint64_t offset, uint64_t n, uint32_t* keys, uint32_t* values,

@@ -145,15 +145,6 @@ struct RegionRouter {  // region of the key's FIRST bucket: floor(h0(k) * R / m)
   }
 };
 
-struct GroupRouter {  // group of the key's first bucket's fine region: (h0(k) >> region_log2) / per, division by multiplication
-  HashFn h0;
-  uint32_t region_log2;
-  uint32_t inv_per;  // floor(2^32 / per) + 1: exact quotient for fine ids < 2^18 and per <= 128
-  __device__ __forceinline__ uint32_t operator()(uint32_t key) const {
-    return static_cast<uint32_t>((static_cast<uint64_t>(bucket_index(h0, key) >> region_log2) * inv_per) >> 32);
-  }
-};
-
 __device__ __forceinline__ uint4 load4(const uint32_t* p, uint64_t i, uint64_t n, bool aligned) {
   if (aligned && i + 4 <= n) return __ldcs(reinterpret_cast<const uint4*>(p + i));
   uint4 r = make_uint4(0, 0, 0, 0);
@@ -372,17 +363,6 @@ cudaError_t launch_region_route(const HashFn& h0, uint32_t n_regions, const uint
   r.mult = static_cast<uint32_t>((static_cast<uint64_t>(n_regions) << 32) / h0.range);  // n_regions < range
   return route<RegionRouter, true, false>(r, n_regions, keys, values, n, scratch8, counts, cursors, out_pairs, nullptr, nullptr,
                                           sm_count, stream);
-}
-
-cudaError_t launch_group_route(const HashFn& h0, uint32_t region_log2, uint32_t per, uint32_t n_groups, const uint32_t* keys,
-                               const uint32_t* values, uint64_t n, uint8_t* scratch8, unsigned long long* counts,
-                               unsigned long long* cursors, uint32_t* out_pairs, int sm_count, cudaStream_t stream) {
-  GroupRouter r;
-  r.h0 = h0;
-  r.region_log2 = region_log2;
-  r.inv_per = static_cast<uint32_t>((1ull << 32) / per) + 1u;
-  return route<GroupRouter, true, false>(r, n_groups, keys, values, n, scratch8, counts, cursors, out_pairs, nullptr, nullptr,
-                                         sm_count, stream);
 }
 
 // ---- K9 ----------------------------------------------------------------------------------------
