@@ -20,7 +20,7 @@ for w in $WHAT; do
           python bench.py --steps 1 --warmup 3 --no-cpu-baseline > $OUT/ncu_find.log 2>&1
       timeout 900 ncu --set full --clock-control none --import-source on -k regex:bulk_insert -s 3 -c 1 -f -o $OUT/prof_insert \
           python bench.py --steps 1 --warmup 3 --no-cpu-baseline > $OUT/ncu_insert.log 2>&1
-      timeout 900 ncu --set full --clock-control none --import-source on -k regex:"route_|bin_split|region_build" -s 15 -c 5 -f -o $OUT/prof_route \
+      timeout 900 ncu --set full --clock-control none --import-source on -k regex:"group_scatter|bin_split|region_build" -s 9 -c 3 -f -o $OUT/prof_route \
           python bench.py --steps 1 --warmup 3 --no-cpu-baseline > $OUT/ncu_route.log 2>&1
       ls -la $OUT;;
     *) echo "unknown step $w";;
