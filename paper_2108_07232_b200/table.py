@@ -297,7 +297,8 @@ class HashTable:
 
     def set_blocked_insert(self, mode) -> None:
         """Blocked builds of device-resident inserts: 0 / False = never (caller order), 1 / True = when the sizes
-        make it pay (default), 2 = always the L2-routed build, 3 = always the shared-memory-blocked build."""
+        make it pay (default: shared-memory-blocked for bcht, L2-routed for 1cht), 2 = always the L2-routed build,
+        3 = always the shared-memory-blocked build.  bp2ht / iht always insert in caller order."""
         _check(self._lib.bht_set_blocked_insert(self._h, int(mode)))
 
     # -- the hot path
