@@ -233,3 +233,49 @@ def test_device_key_generator_and_shard_routing(bht):
         out = torch.empty(k.size, dtype=torch.int32, device="cuda")
         ops.unpermute(dev(pv), dev(idx.astype(np.uint32)), out)
         assert np.array_equal(host(out), v)
+
+
+@pytest.mark.parametrize("b,skew_regions", [(16, 2), (8, 1), (32, 3)])
+def test_blocked_build_with_skewed_first_buckets(bht, ora, b, skew_regions):
+    """The shared-memory-blocked build sizes its group segments, bins and stash for a uniform hash (mean + 6 sigma).  A key
+    set whose first buckets crowd into a few regions overflows all three; the surplus must take the spill list and the
+    general kernel, and the table must still hold exactly the inserted set (csrc/build_blocked.cu)."""
+    n = 150_001
+    cfg = bht.make_config("bcht", n, 0.85, b, seed=bht.mix_seed(41, b))
+    region_buckets = (64 * 1024) // (8 * b)
+    pool = unique_keys(6 * n, 500 + b)
+    h0 = host(bht.hash_keys(int(cfg.alpha[0]), int(cfg.beta[0]), int(cfg.range[0]), dev(pool)))
+    crowded = pool[h0 < skew_regions * region_buckets]
+    spread = pool[h0 >= skew_regions * region_buckets]
+    k_crowded = min(crowded.size, int(0.85 * skew_regions * region_buckets * b * 1.5))  # 1.5x what those regions can hold
+    keys = np.concatenate([crowded[:k_crowded], spread[:n - k_crowded]])
+    np.random.Generator(np.random.MT19937(7)).shuffle(keys)
+    values = random_values(n, 9 * b)
+    table = bht.HashTable(cfg, 0)
+    table.set_blocked_insert(3)
+    o = table.insert(dev(keys), dev(values))
+    assert o.attempted == n and o.inserted + o.failed == n
+    assert table.occupied_slots() == o.inserted and table.count_inadmissible() == 0
+    got = host(table.find(dev(keys)))
+    if o.success:
+        assert np.array_equal(got, values)
+        assert np.array_equal(stored(table), packed(keys, values))
+        otab = ora.table(to_oracle_cfg(cfg))
+        otab.upload_store(table.download_store())
+        assert otab.check_admissibility() == 0
+        want, hits, probes = otab.find_bulk(keys)
+        assert hits == n and np.array_equal(want, values)
+    else:  # dropped pairs are reported and are exactly the ones that are not found
+        dropped = table.failed_keys()
+        assert dropped.size == o.failed
+        missing = keys[got == EMPTY]
+        assert np.array_equal(np.sort(missing), np.sort(dropped))
+    # the same key set into a NON-empty table (region_build loads the regions, finds the loads, claims after them)
+    table2 = bht.HashTable(cfg, 0)
+    table2.set_blocked_insert(3)
+    half = n // 2
+    o1 = table2.insert(dev(keys[:half]), dev(values[:half]))
+    o2 = table2.insert(dev(keys[half:]), dev(values[half:]))
+    assert table2.occupied_slots() == o1.inserted + o2.inserted and table2.count_inadmissible() == 0
+    if o1.success and o2.success:
+        assert np.array_equal(host(table2.find(dev(keys))), values)
