@@ -188,7 +188,7 @@ bht_status bht_set_iht_prose_fallback(bht_table* table, int32_t enabled);
  * result set, different concurrent order).  bcht: the pairs are partitioned in two streaming passes by the 64 KiB
  * region of their first bucket, every region is built in shared memory (slot claims by shared-memory atomics, the
  * first eviction of a pair whose bucket is full included) and only the evicted victims walk on through the general
- * kernel.  1cht, and bcht tables beyond 4 GB: the pairs are routed by L2-sized region and inserted by the general
+ * kernel.  1cht, and bcht tables beyond 8 GB: the pairs are routed by L2-sized region and inserted by the general
  * kernel in that order.  mode 0 = never (caller order), 1 = when the sizes make it pay (default), 2 = always the
  * L2-routed build, 3 = always the shared-memory-blocked build (2 and 3 also on small tables; used by the parity
  * tests).  bp2ht / iht are never blocked: their balanced placements depend on the arrival order, and arrival in

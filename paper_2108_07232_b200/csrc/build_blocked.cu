@@ -416,7 +416,10 @@ BlockedPlan plan_blocked_build(const TableView& t, uint64_t n) {
   uint32_t b_log2 = 0;
   while ((1u << b_log2) < t.bucket_size) ++b_log2;
   if (b_log2 > 6 || n == 0 || n > 0xFFFFFFFFull) return p;
-  uint32_t region_bytes_log2 = kRegionBytesLog2;  // 64 KiB of slots per fine region
+  // 64 KiB of slots per fine region (three CTAs of K11 per SM); 128 KiB (one CTA per SM, ~20 % slower) for tables
+  // between 4 and 8 GB, so that two partition levels of <= 256 x 256 still reach every region
+  uint32_t region_bytes_log2 = kRegionBytesLog2;
+  if ((t.num_buckets << (b_log2 + 3)) > (256ull * kMaxShards << kRegionBytesLog2)) region_bytes_log2 = kRegionBytesLog2 + 1;
   if (const char* e = std::getenv("BHT_REGION_BYTES_LOG2")) region_bytes_log2 = static_cast<uint32_t>(std::atoi(e));  // tuning knob
   if (region_bytes_log2 < 12 || region_bytes_log2 > 17 || region_bytes_log2 < 3 + b_log2 + 5) return p;
   const uint32_t region_log2 = region_bytes_log2 - 3 - b_log2;
