@@ -62,16 +62,21 @@ struct DeviceScope {  // every call runs on the table's device and leaves the ca
   if (scope__.err != cudaSuccess) return cuda_fail(scope__.err, "cudaSetDevice")
 
 constexpr int kStageSlots = 3;
-constexpr uint64_t kStageChunk = 1ull << 22;  // keys per staged chunk: 16 MiB per array over PCIe
+constexpr uint64_t kStageChunk = 1ull << 22;  // keys per staged chunk: 16 MiB per array over PCIe (measured: 2^19..2^24 — 2^22 is the fastest)
 constexpr uint64_t kStageChunkMin = 1ull << 18;
 
 // Length of the staged chunk that starts at `off`: chunks double from kStageChunkMin up to kStageChunk and halve
 // again towards the end, so the pipeline fills and drains in ~1 MiB steps (the first copy-in and the last
 // kernel / copy-out are the only parts of a host-buffer call that nothing overlaps).
 uint64_t stage_chunk_len(uint64_t off, uint64_t n) {
+  static const uint64_t chunk_max = [] {  // BHT_STAGE_CHUNK_LOG2: tuning knob, 18..22
+    const char* e = std::getenv("BHT_STAGE_CHUNK_LOG2");
+    const long v = e ? std::atol(e) : 22;
+    return 1ull << (v < 18 ? 18 : (v > 22 ? 22 : v));
+  }();
   const uint64_t up = std::max(kStageChunkMin, off);
   const uint64_t down = std::max(kStageChunkMin, (n - off) / 2);
-  return std::min(std::min(kStageChunk, n - off), std::min(up, down));
+  return std::min(std::min(chunk_max, n - off), std::min(up, down));
 }
 constexpr uint64_t kFailedLogCap = 1ull << 20;
 constexpr uint32_t kRetryCap = 1024;
