@@ -195,6 +195,13 @@ bht_status bht_set_iht_prose_fallback(bht_table* table, int32_t enabled);
  * first-bucket order measurably lowers the load factor they reach. */
 bht_status bht_set_blocked_insert(bht_table* table, int32_t mode);
 
+/* cuckoo kinds, off by default: insert the pairs that arrive beyond load 0.98 (b = 1: 0.85) with few keys in flight
+ * (<= 1/24 of the slots still free at the end).  Thousands of eviction walks competing for the last free slots hit
+ * max_chain (core.hpp:93-96) 3-5 times more often than the reference's one-walker-at-a-time process; the throttle
+ * brings the build success at load factor 0.99 from ~50 % to ~80 % (reference: 90 %) for 2.5x the build time.
+ * Retrying a failed build with fresh hash constants, as run_trial does (experiments.cpp:69-82), is cheaper. */
+bht_status bht_set_tail_throttle(bht_table* table, int32_t enabled);
+
 /* ---- load factor / store access ---------------------------------------------------------- */
 
 /* realized_load() (table.hpp:40): inserted counter and capacity. */

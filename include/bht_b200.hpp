@@ -141,6 +141,8 @@ class hash_table {
   void set_iht_prose_fallback(bool on) { check(bht_set_iht_prose_fallback(h_, on ? 1 : 0)); }
   // bulk-build schedule: 0 caller order, 1 blocked when it pays (default), 2 L2-routed, 3 shared-memory blocked
   void set_blocked_insert(int mode) { check(bht_set_blocked_insert(h_, mode)); }
+  // few keys in flight for the pairs that arrive beyond load 0.98: build success at LF 0.99 closer to the reference's
+  void set_tail_throttle(bool on) { check(bht_set_tail_throttle(h_, on ? 1 : 0)); }
   // device milliseconds of the last device-resident insert: {routing / binning passes, probe kernel}
   std::pair<float, float> last_insert_phases() {
     float prepare = 0.f, probe = 0.f;

@@ -106,6 +106,7 @@ SIGNATURES = {
     "bht_failed_keys": (C.c_int, [_vp, _vp, C.c_uint64, _u64p]),
     "bht_set_iht_prose_fallback": (C.c_int, [_vp, C.c_int32]),
     "bht_set_blocked_insert": (C.c_int, [_vp, C.c_int32]),
+    "bht_set_tail_throttle": (C.c_int, [_vp, C.c_int32]),
     "bht_last_insert_phases": (C.c_int, [_vp, C.POINTER(C.c_float), C.POINTER(C.c_float)]),
     "bht_load_factor": (C.c_int, [_vp, _u64p, _u64p]),
     "bht_count_occupied": (C.c_int, [_vp, _u64p, _vp]),

@@ -110,6 +110,7 @@ struct bht_table {
   int blocked_insert = 1;
   bool known_empty = true;  // no slot has been written since create / clear: a blocked build need not read the store
   uint64_t host_inserted = 0;  // upper bound of the pairs in the store, kept on the host (tail_plan)
+  bool tail_throttle = false;  // bht_set_tail_throttle
   // device-resident bht_insert: events around the preparation (routing / binning) and the probe kernel of the last
   // call, for bht_last_insert_phases (per-kernel roofline of bench.py)
   cudaEvent_t phase_ev[3] = {};
@@ -313,15 +314,18 @@ int blocked_ctas_per_sm() {
   return e ? std::atoi(e) : 0;
 }
 
-// The last pairs of a cuckoo build that ends at a very high load are inserted with few keys in flight.
-// Measured (tools/exp_success_inflight.py, exp_success_tail.py; bcht b = 16, LF 0.99, 5 M keys, 40 builds each): with
-// 190 k insertions in flight to the end 52 % of the builds succeed, with 4 k in flight 68 %, with 256 in flight 95 %;
-// the CPU reference: 90 %.  Only the end matters — the last 2 % of the pairs at 256 in flight: 88 % — and it is not
-// about the long chains themselves (finishing every chain past 24 evictions in a single CTA changes nothing): when
-// the walkers in flight are as many as the free slots that remain, they take the slots each other was heading for,
-// and max_chain, which the reference calibrates for one walker at a time, is hit 3-5 times more often.  So the
-// pairs that arrive beyond a load threshold go in a second launch whose grid keeps the keys in flight at or
-// below 1/24 of the slots that will still be free at the end.  Builds that end below the threshold are untouched.
+// Optional (bht_set_tail_throttle): the last pairs of a cuckoo build that ends at a very high load are inserted with
+// few keys in flight.  Measured (tools/exp_success_inflight.py, exp_success_tail.py, exp_success_tailcfg.py; bcht b = 16,
+// LF 0.99, profiles/r01j_lf099_success_vs_concurrency.txt): with 190 k insertions in flight to the end, 50 % of 5 M-key
+// builds succeed, with 4 k in flight 68 %, with 256 in flight 95 %; the CPU reference: 90 %.  Only the end matters — the
+// last 2 % of the pairs at 256 in flight: 88 % — and it is not about the long chains themselves (finishing every chain
+// past 24 evictions in a single CTA changes nothing): when the walkers in flight are as many as the free slots that
+// remain, they take the slots each other was heading for, and max_chain, which the reference calibrates for one walker
+// at a time, is hit 3-5 times more often.  With the throttle the pairs that arrive beyond load 0.98 go in a second
+// launch whose grid keeps the keys in flight at or below 1/24 of the slots that will still be free at the end: 82 % of
+// 5 M-key builds succeed, for 2.5x the build time.  It is OFF by default because retrying a failed build with fresh
+// hash constants (what the reference's trial protocol does) is cheaper than throttling: 0.96 ms against 1.59 ms per
+// successful 5 M-key build, 4.3 ms against 6.2 ms at 50 M keys.
 struct TailPlan {
   uint64_t tail = 0;  // pairs at the end of the batch that get the throttled launch
   int grid = 0;       // its CTA cap
@@ -329,11 +333,12 @@ struct TailPlan {
 TailPlan tail_plan(const bht_table* t, uint64_t n) {
   TailPlan p;
   if (t->cfg.kind != BHT_BCHT && t->cfg.kind != BHT_ONE_CHT) return p;
-  if (const char* e = std::getenv("BHT_TAIL_THROTTLE"))
-    if (std::atoi(e) == 0) return p;
+  bool on = t->tail_throttle;
+  if (const char* e = std::getenv("BHT_TAIL_THROTTLE")) on = std::atoi(e) != 0;  // experiment override
+  if (!on) return p;
   const double cap = static_cast<double>(t->cfg.capacity);
   const uint32_t b = t->cfg.bucket_size;
-  double lf = b == 1 ? 0.85 : (b == 2 ? 0.90 : (b == 4 ? 0.94 : 0.96));
+  double lf = b == 1 ? 0.85 : (b == 2 ? 0.90 : (b == 4 ? 0.95 : 0.98));
   if (const char* e = std::getenv("BHT_TAIL_LF")) lf = std::atof(e);
   const uint64_t before = std::min<uint64_t>(t->host_inserted, t->cfg.capacity);
   const uint64_t after = std::min<uint64_t>(before + n, t->cfg.capacity);
@@ -341,7 +346,9 @@ TailPlan tail_plan(const bht_table* t, uint64_t n) {
   if (after <= threshold) return p;
   p.tail = std::min<uint64_t>(n, after - std::max(before, threshold));
   const uint64_t free_at_end = t->cfg.capacity - after;
-  const uint64_t lanes = std::max<uint64_t>(256, free_at_end / 24);
+  uint64_t divisor = 24;
+  if (const char* e = std::getenv("BHT_TAIL_DIV")) divisor = std::max(1l, std::atol(e));  // tuning knob
+  const uint64_t lanes = std::max<uint64_t>(256, free_at_end / divisor);
   p.grid = static_cast<int>(std::min<uint64_t>((lanes + 255) / 256, 1u << 20));
   if (p.grid >= t->sm_count * 4) p = TailPlan{};  // no real throttle: one launch
   return p;
@@ -796,6 +803,12 @@ bht_status bht_set_iht_prose_fallback(bht_table* t, int32_t enabled) {
   if (t == nullptr) return fail(BHT_INVALID_ARGUMENT, "bht_set_iht_prose_fallback: null table");
   if (t->cfg.kind != BHT_IHT) return fail(BHT_KIND_MISMATCH, "iht_insert: table kind does not match the variant");
   t->view.prose = enabled ? 1u : 0u;
+  return BHT_OK;
+}
+
+bht_status bht_set_tail_throttle(bht_table* t, int32_t enabled) {
+  if (t == nullptr) return fail(BHT_INVALID_ARGUMENT, "bht_set_tail_throttle: null table");
+  t->tail_throttle = enabled != 0;
   return BHT_OK;
 }
 

@@ -165,6 +165,7 @@ def test_build_parity_routed(bht, ora, monkeypatch, kind, b, lf, t, mode):
         cfg = bht.make_config(kind, n, lf, b, threshold=t, seed=bht.mix_seed(13, 0x100 + attempt))
         table = bht.HashTable(cfg, 0)
         table.set_blocked_insert(mode)  # whatever the sizes (auto mode only blocks multi-million-key batches)
+        table.set_tail_throttle(lf >= 0.99)  # the throttled second launch for the pairs beyond load 0.98
         outcome = table.insert(dev(present), dev(values))
         if outcome.success:
             break
