@@ -22,6 +22,7 @@
 #define BHT_B200_HPP_
 
 #include <cstdint>
+#include <cstdio>
 #include <optional>
 #include <stdexcept>
 #include <string>
@@ -386,6 +387,86 @@ inline trial_outcome run_trial(const trial_cell& cell) {
   for (std::size_t r = 0; r < cell.positive_ratios.size(); ++r)
     out.find_mean_probes[r] = find_ops[r] ? static_cast<double>(find_probes[r]) / static_cast<double>(find_ops[r]) : 0.0;
   return out;
+}
+
+// run_success_rate (experiments.hpp:115-137, experiments.cpp:114-146): `success_trials` builds per load factor with fresh
+// hash constants mix_seed(cell_seed(seed, cell), t); max_load_factor = the highest grid point with >= 99 % successes.
+struct success_rate_point {
+  double lf = 0.0;
+  double realized_lf = 0.0;
+  unsigned successes = 0;
+  unsigned trials = 0;
+  double fraction() const { return trials == 0 ? 0.0 : static_cast<double>(successes) / trials; }
+};
+struct success_rate_result {
+  std::vector<success_rate_point> points;
+  std::optional<double> max_load_factor;
+};
+inline std::uint64_t cell_seed(std::uint64_t base, std::uint64_t cell_index) { return mix_seed(base, 0x63656c6cull + cell_index); }
+
+inline success_rate_result run_success_rate(const kind_params& params, std::uint64_t n, const std::vector<double>& lf_grid,
+                                            unsigned success_trials, std::uint64_t seed,
+                                            std::optional<std::uint32_t> max_chain = std::nullopt, build_options opts = {}) {
+  success_rate_result result;
+  const key_set keys = generate_keys(mix_seed(seed, 0x6b657973ull), n, opts.device);
+  for (std::size_t cell = 0; cell < lf_grid.size(); ++cell) {
+    success_rate_point point;
+    point.lf = lf_grid[cell];
+    point.trials = success_trials;
+    for (unsigned t = 0; t < success_trials; ++t) {
+      table_config cfg = make_config(params.kind, n, point.lf, params.bucket_size, params.threshold_slots(),
+                                     mix_seed(cell_seed(seed, cell), t), max_chain);
+      point.realized_lf = static_cast<double>(n) / static_cast<double>(cfg.capacity);
+      auto built = build(keys.keys.data(), n, cfg, opts);
+      point.successes += built.second.success;
+    }
+    result.points.push_back(point);
+  }
+  for (const auto& point : result.points)
+    if (point.fraction() >= 0.99 && (!result.max_load_factor || point.lf > *result.max_load_factor)) result.max_load_factor = point.lf;
+  return result;
+}
+
+// One record per (cell, op, positive ratio) and its CSV line (experiments.hpp:62-82, experiments.cpp:232-243).
+struct result_record {
+  table_kind kind = table_kind::bcht;
+  std::uint32_t b = 0;
+  std::optional<std::uint32_t> threshold_pct;
+  std::uint64_t n = 0;
+  double realized_lf = 0.0;
+  std::string op;  // "insert", "find" or "build"
+  std::optional<double> positive_ratio;
+  double mean_probes = 0.0;
+  double ops_per_sec = 0.0;
+  unsigned successes = 0;
+  unsigned failures = 0;
+  std::uint64_t seed = 0;
+  bool budget_exhausted = false;
+};
+inline constexpr const char* result_csv_header =
+    "kind,b,threshold_pct,n,realized_lf,op,positive_ratio,mean_probes,ops_per_sec,successes,failures,seed";
+inline const char* to_string(table_kind kind) {
+  switch (kind) {
+    case table_kind::one_cht: return "1cht";
+    case table_kind::bcht: return "bcht";
+    case table_kind::bp2ht: return "bp2ht";
+    case table_kind::iht: return "iht";
+  }
+  return "?";
+}
+inline std::string format_double(double v) {
+  char buf[64];
+  std::snprintf(buf, sizeof(buf), "%.6g", v);
+  return buf;
+}
+inline std::string csv_line(const result_record& r) {
+  std::string s = std::string(to_string(r.kind)) + ',' + std::to_string(r.b) + ',';
+  if (r.threshold_pct) s += std::to_string(*r.threshold_pct);
+  s += ',' + std::to_string(r.n) + ',' + format_double(r.realized_lf) + ',' + r.op + ',';
+  if (r.positive_ratio) s += format_double(*r.positive_ratio);
+  s += ',' + format_double(r.mean_probes) + ',' + format_double(r.ops_per_sec) + ',' + std::to_string(r.successes) + ',' +
+       std::to_string(r.failures) + ',' + std::to_string(r.seed);
+  return s;
 }
 
 }  // namespace gpu

@@ -144,6 +144,21 @@ int main(int argc, char** argv) {
     trial_outcome h = run_trial(hard);
     CHECK(h.budget_exhausted && h.successes == 0 && h.failures == 5);
   }
+  // success rate far below / above a variant's threshold (test_experiments.cpp:192-198) and the CSV line format
+  {
+    auto r = run_success_rate({table_kind::bcht, 16, 80}, 5000, {0.01, 0.5}, 20, 7);
+    CHECK(r.points.size() == 2 && r.points[0].fraction() == 1.0 && r.points[1].fraction() == 1.0);
+    CHECK(r.max_load_factor && *r.max_load_factor == 0.5);
+    auto hard = run_success_rate({table_kind::bp2ht, 16, 80}, 5000, {0.5, 1.0}, 5, 7);
+    CHECK(hard.points[0].successes == 5 && hard.points[1].successes == 0 && *hard.max_load_factor == 0.5);
+    result_record rec;
+    rec.kind = table_kind::iht; rec.b = 16; rec.threshold_pct = 75; rec.n = 3000; rec.realized_lf = 0.797872; rec.op = "find";
+    rec.positive_ratio = 0.0; rec.mean_probes = 3.0; rec.ops_per_sec = 1.5e7; rec.successes = 2; rec.failures = 0; rec.seed = 42;
+    CHECK(csv_line(rec) == "iht,16,75,3000,0.797872,find,0,3,1.5e+07,2,0,42");
+    rec.kind = table_kind::bcht; rec.threshold_pct.reset(); rec.op = "insert"; rec.positive_ratio.reset(); rec.mean_probes = 1.10823;
+    CHECK(csv_line(rec) == "bcht,16,,3000,0.797872,insert,,1.10823,1.5e+07,2,0,42");
+    CHECK(std::string(result_csv_header) == "kind,b,threshold_pct,n,realized_lf,op,positive_ratio,mean_probes,ops_per_sec,successes,failures,seed");
+  }
   // set_blocked_insert is part of the handle API (host batches are always staged in caller order; the device-resident
   // schedules are covered by tests/test_gpu_parity.py::test_build_parity_routed)
   {
