@@ -1,8 +1,8 @@
-"""Randomised parity sweep of the bulk-build schedules (not part of the test suite: run on the GPU box for a few minutes).
+"""Randomised parity sweep of the bulk-build schedules (under tests/ because it uses the CPU oracle as its checker; not collected by pytest: run on the GPU box for a few minutes, `python tests/fuzz_builds.py [seed] [seconds]`).
 For random (kind, b, load factor, n, schedule, batches): the stored multiset equals the inserted set, every pair is
 admissible, finds answer exactly — checked with the CPU oracle reading the GPU's store."""
 import os, sys, time
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))  # repo root
 import numpy as np
 import torch
 import paper_2108_07232_b200 as bht

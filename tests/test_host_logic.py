@@ -191,3 +191,7 @@ def test_product_never_imports_the_oracle():
                     for line in text.splitlines() if "oracle" in line.lower()), os.path.join(dirpath, f)
     for f in os.listdir(os.path.join(ROOT, "include")):
         assert "oracle/" not in open(os.path.join(ROOT, "include", f)).read()
+    for f in os.listdir(os.path.join(ROOT, "tools")):  # measurement scripts run the product, never the checker
+        path = os.path.join(ROOT, "tools", f)
+        if os.path.isfile(path) and f.endswith(".py"):
+            assert "from oracle" not in open(path).read() and "import oracle" not in open(path).read(), path
