@@ -285,8 +285,8 @@ uint32_t blocked_regions(const bht_table* t, uint64_t n) {
 }
 
 // Plan of a shared-memory-blocked build (build_blocked.cu) of n device-resident pairs, n_regions == 0 when it is
-// not used: the default for large cuckoo batches (1.27 ms against 1.81 ms for the L2-routed build, bcht b = 16,
-// 50 M pairs, LF 0.9); tables beyond 2 GB of slots (more than 256 x 128 fine regions) take the L2-routed build.
+// not used: the default for large bcht batches (1.06 ms against 1.81 ms for the L2-routed build, b = 16, 50 M pairs,
+// LF 0.9); tables beyond 8 GB of slots (more than 256 x 256 fine regions of 128 KiB) take the L2-routed build.
 BlockedPlan smem_blocked_plan(const bht_table* t, uint64_t n) {
   BlockedPlan none{};
   const bool cuckoo = t->cfg.kind == BHT_BCHT || t->cfg.kind == BHT_ONE_CHT;
