@@ -111,3 +111,106 @@ def test_criterion_6_achievable_load_factors(ex):
 def test_criterion_7_peak_loads_of_the_stable_tables(ex, kind, tpct, b, target, lo, hi):
     got, sr = max_lf(ex, kind, b, tpct, DESK_N, lo, hi, 50, 115)
     assert within(got, target, 0.03), (got, [(p.lf, p.successes) for p in sr.points])
+
+
+# ---- criteria 8-10: the reference's OWN checkers (check_membership, check_admissibility, oracle.cpp:13-54) run on GPU-built
+# ---- stores handed over in the reference's dump layout --------------------------------------------------------------
+
+def safe_lf(kind, b):
+    """acceptance.cpp:257-265."""
+    return {"1cht": 0.80, "bcht": 0.95, "bp2ht": 0.88 if b >= 32 else (0.80 if b == 16 else 0.60),
+            "iht": 0.88 if b >= 32 else (0.82 if b == 16 else 0.62)}[kind]
+
+
+def correctness_suite(ref, cfg, table, keys_host, seed):
+    """correctness_suite (acceptance.cpp:267-281): membership {false negatives, wrong values, false positives} over the
+    keys and as many guaranteed-absent keys, and admissibility, by the reference's code on the GPU table's store."""
+    from conftest import to_oracle_cfg
+    rt = ref.table(to_oracle_cfg(cfg))
+    try:
+        rt.upload_store(table.download_store())
+        report = rt.check_membership(keys_host, len(keys_host), seed)
+        return report == {"false_negatives": 0, "wrong_values": 0, "false_positives": 0} and rt.check_admissibility() == 0
+    finally:
+        rt.close()
+
+
+def test_criterion_8_randomized_correctness_properties(bht, ex, ref, ora):
+    """acceptance.cpp:283-368: 100 random (kind, b, n, load factor, threshold) configurations drawn from mt19937_64(116) as
+    the reference draws them, built in bulk on the GPU (builds alternate caller order / blocked schedules where the
+    reference alternates sequential / 8 workers), all clean; then the early-exit differential on 10^6 mixed queries."""
+    from paper_2108_07232_b200 import workload
+    stream = iter(ora.mt19937_64_stream(116, 4000).tolist())
+    kinds = ["1cht", "bcht", "bp2ht", "iht"]  # table_kind order (core.hpp:43)
+    sizes = [8, 16, 32]
+    configs = clean = 0
+    while configs < 100:
+        kind = kinds[next(stream) % 4]
+        b = 1 if kind == "1cht" else sizes[next(stream) % 3]
+        n = 2000 + next(stream) % 50000
+        lf = 0.30 + (safe_lf(kind, b) - 0.30) * ((next(stream) % 1000) / 999.0)
+        tpct = 20 + 20 * (next(stream) % 4)
+        parallel = configs % 2 == 1
+        configs += 1
+        keys = workload.generate_keys(next(stream), n, device=0)
+        threshold = max(1, b * tpct // 100) if kind == "iht" else None
+        cfg = bht.make_config(kind, n, lf, b, threshold=threshold, seed=next(stream))
+        table = bht.HashTable(cfg, 0)
+        table.set_blocked_insert(3 if parallel else 0)
+        d_keys = keys.keys.view(torch.int32)
+        outcome = table.insert(d_keys, bht.values_for_keys(d_keys))
+        assert outcome.success, (kind, b, lf, n)   # every configuration is at or below its variant's safe load factor
+        clean += correctness_suite(ref, cfg, table, keys.keys.cpu().numpy(), next(stream))
+        table.close()
+    assert clean == configs == 100
+    keys = workload.generate_keys(117, DESK_N, device=0)
+    d_keys = keys.keys.view(torch.int32)
+    for attempt in range(20):
+        cfg = bht.make_config("bcht", DESK_N, 0.98, 16, seed=117 if attempt == 0 else 118 + attempt)
+        table, outcome = bht.build(d_keys, cfg, device=0)
+        if outcome.success:
+            break
+    assert outcome.success
+    q = torch.from_numpy(workload.generate_queries(keys, 0.5, DESK_N, 119, device=0).keys.view(np.int32)).cuda()
+    assert torch.equal(table.find(q, as_kind="bcht"), table.find_exhaustive(q))
+
+
+@pytest.mark.parametrize("kind,b,threshold", [("1cht", 1, None), ("bcht", 16, None), ("bp2ht", 32, None), ("iht", 32, 25)])
+def test_criterion_9_concurrent_builds(bht, ref, kind, b, threshold):
+    """acceptance.cpp:371-423: a concurrent build of 10^6 keys at LF 0.8 is clean under the reference's checkers; for the
+    stable tables, pairs recorded right after their own batch never move while seven more batches are inserted."""
+    from paper_2108_07232_b200 import workload
+    keys = workload.generate_keys(120 + b, DESK_N, device=0)
+    cfg = bht.make_config(kind, DESK_N, 0.8, b, threshold=threshold, seed=120 + b)
+    d_keys = keys.keys.view(torch.int32)
+    table, outcome = bht.build(d_keys, cfg, device=0)
+    assert outcome.success
+    assert correctness_suite(ref, cfg, table, keys.keys.cpu().numpy(), 121 + b)
+    if kind in ("bp2ht", "iht"):
+        fresh = bht.HashTable(cfg, 0)
+        host_keys = keys.keys.cpu().numpy()
+        chunk = (DESK_N + 7) // 8
+        where = {}
+        for w in range(8):
+            part = d_keys[w * chunk:(w + 1) * chunk]
+            assert fresh.insert(part, bht.values_for_keys(part)).success
+            store = fresh.download_store()
+            slot_keys = (store & np.uint64(0xFFFFFFFF)).astype(np.uint32)
+            occupied = np.flatnonzero(store != np.uint64(0xFFFFFFFFFFFFFFFF))
+            order = np.argsort(slot_keys[occupied], kind="stable")
+            sorted_keys, sorted_slots = slot_keys[occupied][order], occupied[order]
+            mine = host_keys[w * chunk:(w + 1) * chunk]
+            pos = np.searchsorted(sorted_keys, mine)
+            assert np.array_equal(sorted_keys[pos], mine)
+            where[w] = sorted_slots[pos]
+            for earlier in range(w):   # stability: what was placed by an earlier batch is still exactly there
+                old = host_keys[earlier * chunk:(earlier + 1) * chunk]
+                assert np.array_equal(slot_keys[where[earlier]], old)
+        fresh.close()
+
+
+def test_criterion_10_sector_model_arithmetic(bht):
+    """acceptance.cpp:459-469 (host arithmetic, exact)."""
+    assert bht.predict_sectors("bcht", 16, 1.0, bht.OP_FIND) == 4.0
+    assert bht.predict_sectors("bcht", 16, 3.0, bht.OP_FIND) == 12.0
+    assert bht.predict_sectors("bcht", 16, 1.0, bht.OP_INSERT) == 5.0
