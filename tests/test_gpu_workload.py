@@ -182,3 +182,65 @@ def test_run_experiment_csv_diffs_against_the_reference(ex, ref):
     again = ex.run_experiment(spec)
     for a, b_ in zip(result.records, again.records):
         assert (a.successes, a.failures, a.realized_lf) == (b_.successes, b_.failures, b_.realized_lf)
+
+
+# ---- the remaining cases of proj/tests/test_experiments.cpp ------------------------------------------------------------
+
+def tiny_spec(ex):
+    """tiny_spec (test_experiments.cpp:12-23)."""
+    return ex.ExperimentSpec(scen="probe_analysis", kinds=[ex.KindParams("bcht", 16, 80)], n_grid=[20000], lf_grid=[0.6, 0.8],
+                             positive_ratios=[1.0, 0.0], trials=2, seed=77)
+
+
+def test_every_grid_cell_yields_one_record_per_op_and_ratio(ex):
+    """test_experiments.cpp:63-83."""
+    r = ex.run_experiment(tiny_spec(ex))
+    assert len(r.records) == 6  # 2 lf cells x (1 insert + 2 find ratios)
+    inserts = [rec for rec in r.records if rec.op == "insert"]
+    finds = [rec for rec in r.records if rec.op == "find"]
+    assert len(inserts) == 2 and len(finds) == 4
+    assert all(rec.positive_ratio is None for rec in inserts) and all(rec.positive_ratio is not None for rec in finds)
+    assert all(rec.successes == 2 and rec.mean_probes >= 1.0 for rec in r.records)
+    assert all(rec.mean_probes <= 3.0 for rec in finds)  # h for bcht
+    out = io.StringIO()
+    ex.write_csv(out, r)
+    assert out.getvalue().split("\n")[0] == ex.RESULT_CSV_HEADER  # csv header is pinned (test_experiments.cpp:85-93)
+
+
+def test_probe_means_ignore_query_order(bht, wl):
+    """test_experiments.cpp:95-111."""
+    keys = wl.generate_keys(81, 20000, device=0)
+    cfg = bht.make_config("bcht", 20000, 0.9, 16, seed=81)
+    table, outcome = bht.build(keys.keys.view(torch.int32), cfg, device=0)
+    assert outcome.success
+    q = wl.generate_queries(keys, 0.5, 20000, 82, device=0).keys
+    ordered = table.find(torch.from_numpy(q.view(np.int32)).cuda(), want_stats=True)[1]
+    shuffled_q = q.copy()
+    np.random.Generator(np.random.MT19937(83)).shuffle(shuffled_q)
+    shuffled = table.find(torch.from_numpy(shuffled_q.view(np.int32)).cuda(), want_stats=True)[1]
+    assert ordered.probes == shuffled.probes and ordered.hits == shuffled.hits == 10000
+
+
+@pytest.mark.parametrize("kind", ["1cht", "bcht", "bp2ht", "iht"])
+def test_insertion_probes_respond_to_load_as_each_variant_predicts(ex, kind):
+    """test_experiments.cpp:151-173: nondecreasing in the load factor for the cuckoo variants and iht (slack 0.02),
+    exactly 2 for bp2ht."""
+    prev = 0.0
+    for lf in (0.5, 0.6, 0.7, 0.8):
+        out = ex.run_trial(ex.TrialCell(ex.KindParams(kind, 1 if kind == "1cht" else 16, 80), n=50000, lf=lf, trials=2, seed=90))
+        assert not out.budget_exhausted
+        if kind == "bp2ht":
+            assert out.insert_mean_probes == 2.0
+        else:
+            assert out.insert_mean_probes >= prev - 0.02
+        prev = out.insert_mean_probes
+
+
+def test_probe_means_are_insensitive_to_the_key_count(ex):
+    """test_experiments.cpp:175-190."""
+    means = []
+    for n in (100_000, 1_000_000):
+        out = ex.run_trial(ex.TrialCell(ex.KindParams("bcht", 16, 80), n=n, lf=0.9, trials=3, seed=95))
+        assert not out.budget_exhausted
+        means.append(out.insert_mean_probes)
+    assert abs(means[0] - means[1]) / means[1] < 0.02
