@@ -43,6 +43,11 @@
 
 #include "insert_common.cuh"
 
+#ifndef BHT_BUILD_BLOCK  // measured (insert, 50 M pairs): 192 x 20: 1.087 ms, 256 x 16: 1.062, 320 x 12: 1.034, 384 x 10: 1.034 (spills)
+#define BHT_BUILD_BLOCK 320
+#define BHT_BUILD_U 12
+#endif
+
 namespace bht_b200 {
 
 namespace {
@@ -50,7 +55,7 @@ namespace {
 constexpr int kSplitBlock = 256;
 constexpr int kSplitPerThread = 8;
 constexpr int kSplitTile = kSplitBlock * kSplitPerThread;  // 2048 pairs
-constexpr int kBuildBlock = 256;   // few threads with many loads in flight each: 3 CTAs/SM by shared memory
+constexpr int kBuildBlock = BHT_BUILD_BLOCK;   // few threads with many loads in flight each: 3 CTAs/SM by shared memory
 constexpr uint32_t kStashPairs = 1024;  // per-CTA stash of spilled pairs (K11)
 constexpr uint32_t kRegionBytesLog2 = 16;
 
@@ -312,7 +317,7 @@ region_build_kernel(const __grid_constant__ TableView t, uint32_t region_log2, u
   const uint32_t n_r = min(bin_cursor[region], cap);
   const uint2* bin = bins + static_cast<uint64_t>(region) * cap;
   uint32_t n_ins = 0;
-  constexpr int U = 16;  // pairs in flight per thread: a 64 KiB region holds ~29 pairs per thread at load factor 0.9
+  constexpr int U = BHT_BUILD_U;  // pairs in flight per thread: a 64 KiB region holds ~29 pairs per thread at load factor 0.9
   for (uint32_t i0 = threadIdx.x; i0 - lane < n_r; i0 += kBuildBlock * U) {  // warp-uniform trip count
     uint2 kv[U];
     bool in[U];
