@@ -53,7 +53,10 @@ namespace bht_b200 {
 namespace {
 
 constexpr int kSplitBlock = 256;
-constexpr int kSplitPerThread = 8;
+#ifndef BHT_SPLIT_PER_THREAD
+#define BHT_SPLIT_PER_THREAD 8
+#endif
+constexpr int kSplitPerThread = BHT_SPLIT_PER_THREAD;
 constexpr int kSplitTile = kSplitBlock * kSplitPerThread;  // 2048 pairs
 constexpr int kBuildBlock = BHT_BUILD_BLOCK;   // few threads with many loads in flight each: 3 CTAs/SM by shared memory
 constexpr uint32_t kStashPairs = 1024;  // per-CTA stash of spilled pairs (K11)
@@ -112,16 +115,17 @@ group_scatter_kernel(const __grid_constant__ HashFn h0, uint32_t region_log2, ui
     const uint64_t i0 = tile * kSplitTile;
     hist[threadIdx.x] = 0;
     __syncthreads();
-    uint32_t k[2][4], v[2][4], dst[2][4], rank[2][4];
+    constexpr int kGroups = kSplitPerThread / 4;  // groups of 4 consecutive pairs per thread
+    uint32_t k[kGroups][4], v[kGroups][4], dst[kGroups][4], rank[kGroups][4];
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
+    for (int j = 0; j < kGroups; ++j) {
       const uint64_t i = i0 + (static_cast<uint64_t>(j) * kSplitBlock + threadIdx.x) * 4;
       const uint4 k4 = load_group4(keys, i, n, aligned), v4 = load_group4(values, i, n, aligned);
       k[j][0] = k4.x, k[j][1] = k4.y, k[j][2] = k4.z, k[j][3] = k4.w;
       v[j][0] = v4.x, v[j][1] = v4.y, v[j][2] = v4.z, v[j][3] = v4.w;
     }
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
+    for (int j = 0; j < kGroups; ++j) {
       const uint64_t i = i0 + (static_cast<uint64_t>(j) * kSplitBlock + threadIdx.x) * 4;
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
@@ -148,7 +152,7 @@ group_scatter_kernel(const __grid_constant__ HashFn h0, uint32_t region_log2, ui
     }
     __syncthreads();
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
+    for (int j = 0; j < kGroups; ++j) {
       const uint64_t i = i0 + (static_cast<uint64_t>(j) * kSplitBlock + threadIdx.x) * 4;
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
