@@ -109,6 +109,15 @@ class ClockSampler:
         self._thread = threading.Thread(target=self._loop, daemon=True)
         self._thread.start()
 
+    def sample_until(self, event):
+        """Samples from the calling thread while the GPU works towards `event` (a recorded torch.cuda.Event): the steps
+        of the timed region are enqueued asynchronously, so the host is free exactly while the device is under load."""
+        while not event.query():
+            try:
+                self._sample_once()
+            except Exception:  # noqa: BLE001
+                break
+
     def stop(self):
         self._stop.set()
         if self._thread is not None:
@@ -306,6 +315,7 @@ def run_cuda(args):
         for _ in range(args.steps):
             step(timers)
         t_end.record(stream)
+        sampler.sample_until(t_end)
         barrier()
         clocks = sampler.stop()
         launches = bht.kernel_launch_count() - launches0
@@ -444,6 +454,7 @@ def run_cuda(args):
     for _ in range(args.steps):
         step()
     t_end.record(stream)
+    sampler.sample_until(t_end)
     barrier()
     clocks = sampler.stop()
     ms_step = max_over_ranks(t_start.elapsed_time(t_end) / args.steps)
