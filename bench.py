@@ -486,10 +486,31 @@ def load_traffic():
 
 
 def load_peaks():
+    """HBM peak for the roofline: the driver-written MEASURED_PEAKS.json when present (whatever it calls the HBM copy
+    bandwidth; the burst figure when it distinguishes, because every kernel here is timed alone by its own CUDA events),
+    else the profiling recipe's fallback."""
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
-    if os.path.exists(path):
+    try:
         p = json.load(open(path))
-        return {"hbm_gbs": float(p["hbm_gbs"]), "source": "MEASURED_PEAKS.json (measured copy bandwidth)"}
+        flat = {}
+
+        def walk(prefix, node):
+            if isinstance(node, dict):
+                for k, v in node.items():
+                    walk(f"{prefix}.{k}" if prefix else str(k), v)
+            elif isinstance(node, (int, float)) and not isinstance(node, bool):
+                flat[prefix.lower()] = float(node)
+        walk("", p)
+        hbm = {k: v for k, v in flat.items() if "hbm" in k and ("gb" in k or "bw" in k or "bandwidth" in k or "copy" in k)}
+        if hbm:
+            key = next((k for k in hbm if "burst" in k), None) or ("hbm_gbs" if "hbm_gbs" in hbm else sorted(hbm)[0])
+            value = hbm[key]
+            if value > 100000:  # bytes/s rather than GB/s
+                value /= 1e9
+            if 1000.0 < value < 20000.0:
+                return {"hbm_gbs": value, "source": f"MEASURED_PEAKS.json ({key})"}
+    except (OSError, ValueError):
+        pass
     return {"hbm_gbs": 6650.0, "source": "fallback 6.65 TB/s (B200_PROFILING.md)"}
 
 
