@@ -111,6 +111,10 @@ struct bht_table {
   bool known_empty = true;  // no slot has been written since create / clear: a blocked build need not read the store
   uint64_t host_inserted = 0;  // upper bound of the pairs in the store, kept on the host (tail_plan)
   bool tail_throttle = false;  // bht_set_tail_throttle
+  // bp2ht / iht: one 16-bit load counter per bucket for the counter-claimed insert (insert_claim.cu); loads_valid =
+  // the counters describe the store (false after anything else may have written slots: they are rebuilt on demand)
+  uint32_t* loads = nullptr;
+  bool loads_valid = false;
   // device-resident bht_insert: events around the preparation (routing / binning) and the probe kernel of the last
   // call, for bht_last_insert_phases (per-kernel roofline of bench.py)
   cudaEvent_t phase_ev[3] = {};
@@ -254,9 +258,25 @@ cudaError_t launch_insert_kind(bht_table* t, PairSource src, uint64_t n, int max
     case BHT_BCHT:
       return launch_insert_cuckoo(t->view, a);
     case BHT_BP2HT:
-      return launch_insert_p2(t->view, a);
-    case BHT_IHT:
-      return launch_insert_iht(t->view, a);
+    case BHT_IHT: {
+      // Counter-claimed insert (insert_claim.cu) when the store lives in HBM (or when forced, mode 3): the candidates'
+      // loads come from the L2-resident counter array and the only HBM access of an insertion is the 8-byte store.
+      // Small tables keep the bucket-reading kernels (their probes are L2 hits anyway); whatever they write makes the
+      // counters stale, and they are rebuilt from the store before the next counter-claimed launch.
+      const bool big = t->cfg.capacity * sizeof(uint64_t) >= (192ull << 20);
+      const char* env = std::getenv("BHT_CLAIM_INSERT");  // experiment override: 0 = never, 1 = always
+      const bool claim = t->loads != nullptr && (env ? std::atoi(env) != 0 : (t->blocked_insert == 3 || (t->blocked_insert == 1 && big)));
+      if (claim) {
+        if (!t->loads_valid) {
+          e = launch_load_count(t->view, t->loads, t->sm_count, stream);
+          if (e != cudaSuccess) return e;
+          t->loads_valid = true;
+        }
+        return launch_claim_insert(t->view, t->loads, a, t->cfg.kind == BHT_IHT);
+      }
+      t->loads_valid = false;
+      return t->cfg.kind == BHT_BP2HT ? launch_insert_p2(t->view, a) : launch_insert_iht(t->view, a);
+    }
     default: return cudaErrorInvalidValue;
   }
 }
@@ -642,6 +662,11 @@ bht_status bht_create(const bht_config* cfg, int32_t device, bht_table** out) {
   if (e == cudaSuccess) e = cudaMalloc(&t->failed_keys, kFailedLogCap * sizeof(uint32_t));
   if (e == cudaSuccess) e = cudaMalloc(&t->cursors, kCursorSlots * sizeof(uint32_t));
   for (int i = 0; i < 3 && e == cudaSuccess; ++i) e = cudaEventCreate(&t->phase_ev[i]);
+  if (e == cudaSuccess && (cfg->kind == BHT_BP2HT || cfg->kind == BHT_IHT)) {
+    e = cudaMalloc(&t->loads, claim_loads_bytes(cfg->num_buckets));
+    if (e == cudaSuccess) e = cudaMemset(t->loads, 0, claim_loads_bytes(cfg->num_buckets));
+    t->loads_valid = e == cudaSuccess;
+  }
   if (e == cudaSuccess) e = cudaMemset(t->ctr, 0, sizeof(DevCounters));
   if (e == cudaSuccess) e = launch_fill_empty(store, cfg->capacity, t->sm_count, nullptr);
   if (e == cudaSuccess) e = cudaStreamSynchronize(nullptr);
@@ -686,6 +711,7 @@ bht_status bht_destroy(bht_table* t) {
   cudaFreeHost(t->ctr_host);
   cudaFree(t->failed_keys);
   cudaFree(t->cursors);
+  if (t->loads) cudaFree(t->loads);
   for (cudaEvent_t ev : t->phase_ev)
     if (ev) cudaEventDestroy(ev);
   delete t;
@@ -700,6 +726,10 @@ bht_status bht_clear(bht_table* t, void* stream) {
   BHT_CUDA(cudaMemsetAsync(t->ctr, 0, sizeof(DevCounters), as_stream(stream)));
   t->known_empty = true;
   t->host_inserted = 0;
+  if (t->loads != nullptr) {
+    BHT_CUDA(cudaMemsetAsync(t->loads, 0, claim_loads_bytes(t->cfg.num_buckets), as_stream(stream)));
+    t->loads_valid = true;
+  }
   return BHT_OK;
 }
 
@@ -873,6 +903,7 @@ bht_status bht_upload_store(bht_table* t, const uint64_t* host_src, void* stream
   std::lock_guard<std::mutex> lock(t->mu);
   cudaStream_t s = as_stream(stream);
   t->known_empty = false;
+  t->loads_valid = false;
   BHT_CUDA(cudaMemcpyAsync(t->view.store, host_src, t->cfg.capacity * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
   BHT_CUDA(cudaMemsetAsync(t->ctr, 0, sizeof(DevCounters), s));
   BHT_CUDA(launch_count_occupied(t->view.store, t->cfg.capacity, &t->ctr->inserted_total, t->sm_count, s));
@@ -907,6 +938,7 @@ bht_status bht_dump_store(const bht_table* t, const char* path) {
 uint64_t* bht_device_store(const bht_table* t) {
   if (t == nullptr) return nullptr;
   const_cast<bht_table*>(t)->known_empty = false;  // the caller may write slots behind the library's back
+  const_cast<bht_table*>(t)->loads_valid = false;
   return t->view.store;
 }
 

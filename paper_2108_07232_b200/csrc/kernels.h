@@ -45,6 +45,12 @@ cudaError_t launch_insert_cuckoo(const TableView& t, const InsertLaunch& a);
 cudaError_t launch_insert_p2(const TableView& t, const InsertLaunch& a);
 cudaError_t launch_insert_iht(const TableView& t, const InsertLaunch& a);
 
+// insert_claim.cu — K12 (bp2ht) / K13 (iht): counter-claimed insert.  `loads`: one 16-bit load counter per bucket
+// (claim_loads_bytes), exact for the store (zero for an empty one, else rebuilt by launch_load_count).
+size_t claim_loads_bytes(uint64_t num_buckets);
+cudaError_t launch_load_count(const TableView& t, uint32_t* loads, int sm_count, cudaStream_t stream);
+cudaError_t launch_claim_insert(const TableView& t, uint32_t* loads, const InsertLaunch& a, bool iht);
+
 // build_blocked.cu — K10 bin_scatter + K11 region_build: the shared-memory-blocked first pass of a cuckoo build.
 constexpr uint32_t kMaxBlockedRegions = 40000;  // 16-bit region ids, histogram of one tile in shared memory
 struct BlockedPlan {
