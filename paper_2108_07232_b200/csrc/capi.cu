@@ -111,7 +111,7 @@ struct bht_table {
   bool known_empty = true;  // no slot has been written since create / clear: a blocked build need not read the store
   uint64_t host_inserted = 0;  // upper bound of the pairs in the store, kept on the host (tail_plan)
   bool tail_throttle = false;  // bht_set_tail_throttle
-  // bp2ht / iht: one 16-bit load counter per bucket for the counter-claimed insert (insert_claim.cu); loads_valid =
+  // bp2ht / iht: one 32-bit load counter per bucket for the counter-claimed insert (insert_claim.cu); loads_valid =
   // the counters describe the store (false after anything else may have written slots: they are rebuilt on demand)
   uint32_t* loads = nullptr;
   bool loads_valid = false;

@@ -4,16 +4,18 @@
 // their LOADS (bucket.hpp:26-31); the claim itself is one CAS at slot = load (table.cpp:126,181).  On a 444 MB store
 // that is 2 (bp2ht) or 1-3 (iht) random 128-byte line reads per pair plus the write-back of the claimed sector, and the
 // kernels of insert_p2.cu / insert_iht.cu run at HBM's random-access ceiling (44-48 G accesses/s).  Here the loads live
-// in a side array — one 16-bit counter per bucket, 7 MB for 3.5 M buckets, L2-resident — kept exact by the inserts
+// in a side array — one 32-bit counter per bucket, 14 MB for 3.5 M buckets, L2-resident — kept exact by the inserts
 // themselves:
 //   read the counters of the candidates (L2 hits), decide exactly as the reference does (less loaded, ties to the first
 //   hash function; iht: primary while its load is below t), claim slot = old counter with one atomic on the counter, and
 //   write the pair with one 8-byte store.  The store is the only HBM access of an insertion.
 // The order of the decisions is the caller's order (a sliding window of keys in flight, as in the other kernels), so the
 // placement statistics are those of the reference's process; nothing is grouped by bucket.
-// Claim rules:  bp2ht and iht secondaries — atomicAdd on the counter; a returned value >= b means the bucket filled up
-//   since it was read (the lost-race case of table.cpp:127-129): the lane marks it full and decides again, no probe is
-//   counted twice.  A counter can therefore overshoot b by the number of such late claimers; every reader clamps it.
+// Claim rules:  bp2ht — CAS on the counter from the load that was read to load + 1; a bucket that moved is decided again
+//   with fresh loads (the lost-race case of table.cpp:127-129), no probe is counted twice.
+//   iht secondaries — atomicAdd on the counter; a returned value >= b means the bucket filled up since it was read: the
+//   lane marks it full and decides again.  A counter can therefore overshoot b by the number of such late claimers (at most the keys in flight,
+//   far below 2^32, even when every key of a batch is the same); every reader clamps it.
 //   iht primary — the rule "stay while load < t" (table.cpp:159) is enforced exactly with a CAS on the counter word.
 // The counters are rebuilt from the store (load_count_kernel) whenever something else may have written slots
 // (bht_upload_store, the per-bucket CAS kernels of small batches, bht_device_store).
@@ -29,30 +31,26 @@ namespace {
 
 constexpr int kClaimBlock = 256;
 
-__device__ __forceinline__ uint32_t counter_of(uint32_t word, uint32_t bucket) { return (word >> (16u * (bucket & 1u))) & 0xFFFFu; }
 __device__ __forceinline__ uint32_t read_load(const uint32_t* __restrict__ loads, uint32_t bucket, uint32_t b) {
-  return min(counter_of(__ldcg(loads + (bucket >> 1)), bucket), b);
+  return min(__ldcg(loads + bucket), b);
 }
 // Claims the next slot of `bucket`: returns the slot index, or b when the bucket is (now) full.
 __device__ __forceinline__ uint32_t claim_slot(uint32_t* __restrict__ loads, uint32_t bucket, uint32_t b) {
-  const uint32_t old = atomicAdd(loads + (bucket >> 1), 1u << (16u * (bucket & 1u)));
-  return min(counter_of(old, bucket), b);
+  return min(atomicAdd(loads + bucket, 1u), b);
 }
 // Claims slot = load of `bucket` only while load < limit (iht primary): returns the slot, or the load that stopped it.
 __device__ __forceinline__ uint32_t claim_slot_below(uint32_t* __restrict__ loads, uint32_t bucket, uint32_t limit, uint32_t b,
                                                       bool& claimed) {
-  uint32_t* word = loads + (bucket >> 1);
-  uint32_t old = __ldcg(word);
+  uint32_t old = __ldcg(loads + bucket);
   for (;;) {
-    const uint32_t load = min(counter_of(old, bucket), b);
-    if (load >= limit) {
+    if (old >= limit) {
       claimed = false;
-      return load;
+      return min(old, b);
     }
-    const uint32_t seen = atomicCAS(word, old, old + (1u << (16u * (bucket & 1u))));
+    const uint32_t seen = atomicCAS(loads + bucket, old, old + 1u);
     if (seen == old) {
       claimed = true;
-      return load;
+      return old;
     }
     old = seen;
   }
@@ -71,18 +69,12 @@ __device__ __forceinline__ uint4 load4(const uint32_t* __restrict__ p, uint64_t 
 // load of every bucket = 1 + index of its last occupied slot (compute_load whenever the occupied slots form a prefix)
 __global__ void __launch_bounds__(kClaimBlock)
 load_count_kernel(const uint64_t* __restrict__ store, uint64_t num_buckets, uint32_t b, uint32_t* __restrict__ loads) {
-  const uint64_t n_words = (num_buckets + 1) >> 1;
-  for (uint64_t w = static_cast<uint64_t>(blockIdx.x) * kClaimBlock + threadIdx.x; w < n_words; w += static_cast<uint64_t>(gridDim.x) * kClaimBlock) {
-    uint32_t word = 0;
-    for (uint32_t h = 0; h < 2; ++h) {
-      const uint64_t bucket = 2 * w + h;
-      uint32_t load = 0;
-      if (bucket < num_buckets)
-        for (uint32_t s = 0; s < b; ++s)
-          if (static_cast<uint32_t>(store[bucket * b + s]) != kEmptyKey) load = s + 1;
-      word |= load << (16 * h);
-    }
-    loads[w] = word;
+  for (uint64_t bucket = static_cast<uint64_t>(blockIdx.x) * kClaimBlock + threadIdx.x; bucket < num_buckets;
+       bucket += static_cast<uint64_t>(gridDim.x) * kClaimBlock) {
+    uint32_t load = 0;
+    for (uint32_t s = 0; s < b; ++s)
+      if (static_cast<uint32_t>(store[bucket * b + s]) != kEmptyKey) load = s + 1;
+    loads[bucket] = load;
   }
 }
 
@@ -119,26 +111,46 @@ claim_insert_p2_kernel(const __grid_constant__ TableView t, uint32_t* __restrict
       l0[e] = read_load(loads, b0[e], B);
       l1[e] = read_load(loads, b1[e], B);
     }
+    // The claim is a CAS from the load that was read to load + 1: a bucket that changed in between is decided again with
+    // its fresh load, exactly the lost-race path of table.cpp:127-129.  (A blind atomicAdd would let hundreds of thousands
+    // of keys in flight act on the same stale loads; measured, that costs bp2ht 0.03-0.05 of achievable load factor.)
+    // First one attempt for each of the four keys, all in flight together; then the retries.
+    uint32_t cb[4], cl[4], seen[4];
+    bool tried[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const bool first = l0[e] <= l1[e];  // tie -> first hash function (table.cpp:124)
+      cb[e] = first ? b0[e] : b1[e];
+      cl[e] = first ? l0[e] : l1[e];
+      tried[e] = i + e < n && cl[e] < B;
+      seen[e] = cl[e];
+      if (tried[e]) seen[e] = atomicCAS(loads + cb[e], cl[e], cl[e] + 1u);
+    }
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       if (i + e >= n) continue;
       n_probe += 2;
-      for (;;) {
-        if (l0[e] == B && l1[e] == B) {  // both full: the insertion fails (table.cpp:118-119)
-          ++n_fail;
-          record_failed(ctr, failed_keys, failed_cap, k[e]);
-          break;
+      bool placed = tried[e] && seen[e] == cl[e];
+      while (!placed) {
+        if (tried[e]) {  // the chosen bucket moved: take its fresh load, look at the other one again, decide again
+          const uint32_t fresh = min(seen[e], B);
+          if (cb[e] == b0[e]) l0[e] = fresh, l1[e] = b0[e] == b1[e] ? fresh : read_load(loads, b1[e], B);
+          else l1[e] = fresh, l0[e] = read_load(loads, b0[e], B);
         }
-        const bool first = l0[e] <= l1[e];  // tie -> first hash function (table.cpp:124)
-        const uint32_t cb = first ? b0[e] : b1[e];
-        const uint32_t slot = claim_slot(loads, cb, B);
-        if (slot < B) {
-          store[static_cast<uint64_t>(cb) * B + slot] = pack_pair(k[e], v[e]);
-          ++n_ins;
-          break;
-        }
-        if (first) l0[e] = B; else l1[e] = B;  // filled up since it was read: decide again with what is now known
-        if (b0[e] == b1[e]) l0[e] = l1[e] = B;
+        if (l0[e] == B && l1[e] == B) break;  // both full: the insertion fails (table.cpp:118-119)
+        const bool first = l0[e] <= l1[e];
+        cb[e] = first ? b0[e] : b1[e];
+        cl[e] = first ? l0[e] : l1[e];
+        tried[e] = true;
+        seen[e] = atomicCAS(loads + cb[e], cl[e], cl[e] + 1u);
+        placed = seen[e] == cl[e];
+      }
+      if (placed) {
+        store[static_cast<uint64_t>(cb[e]) * B + cl[e]] = pack_pair(k[e], v[e]);
+        ++n_ins;
+      } else {
+        ++n_fail;
+        record_failed(ctr, failed_keys, failed_cap, k[e]);
       }
     }
   }
@@ -176,14 +188,14 @@ claim_insert_iht_kernel(const __grid_constant__ TableView t, uint32_t* __restric
     for (int e = 0; e < 4; ++e) {
       live[e] = i + e < n;
       pb[e] = bucket_index(t.h[0], k[e]);
-      pw[e] = live[e] ? __ldcg(loads + (pb[e] >> 1)) : 0u;
+      pw[e] = live[e] ? __ldcg(loads + pb[e]) : 0u;
     }
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      pl[e] = min(counter_of(pw[e], pb[e]), B);
+      pl[e] = min(pw[e], B);
       tried[e] = live[e] && pl[e] < t.threshold;  // stays while load < t (table.cpp:159)
       seen[e] = pw[e];
-      if (tried[e]) seen[e] = atomicCAS(loads + (pb[e] >> 1), pw[e], pw[e] + (1u << (16u * (pb[e] & 1u))));
+      if (tried[e]) seen[e] = atomicCAS(loads + pb[e], pw[e], pw[e] + 1u);
     }
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
@@ -248,11 +260,10 @@ claim_insert_iht_kernel(const __grid_constant__ TableView t, uint32_t* __restric
 
 }  // namespace
 
-size_t claim_loads_bytes(uint64_t num_buckets) { return ((num_buckets + 1) >> 1) * sizeof(uint32_t); }
+size_t claim_loads_bytes(uint64_t num_buckets) { return num_buckets * sizeof(uint32_t); }
 
 cudaError_t launch_load_count(const TableView& t, uint32_t* loads, int sm_count, cudaStream_t stream) {
-  const uint64_t words = (t.num_buckets + 1) >> 1;
-  const int grid = static_cast<int>(std::min<uint64_t>((words + kClaimBlock - 1) / kClaimBlock, static_cast<uint64_t>(sm_count) * 8));
+  const int grid = static_cast<int>(std::min<uint64_t>((t.num_buckets + kClaimBlock - 1) / kClaimBlock, static_cast<uint64_t>(sm_count) * 8));
   load_count_kernel<<<grid, kClaimBlock, 0, stream>>>(t.store, t.num_buckets, t.bucket_size, loads);
   note_launch();
   return cudaGetLastError();

@@ -138,6 +138,38 @@ def test_single_bucket_contention_claims_exactly_b(bht):
             assert np.array_equal(v, k ^ np.uint32(0xABCD))  # no torn pairs (test_bucket.cpp:97-124)
 
 
+@pytest.mark.parametrize("kind", ["bp2ht", "iht"])
+def test_hot_buckets_in_a_wide_table_with_counter_claims(bht, kind):
+    """Counter-claimed insert (csrc/insert_claim.cu): every key of a 600 k batch hashes to the same two (three) buckets of
+    a 200 k-bucket table, so hundreds of thousands of lanes claim on the same counters at once.  Exactly the slots of those
+    buckets are won, the counters' overshoot touches no neighbour, and a second batch into the same table places nothing."""
+    nb, b, n = 200_000, 16, 600_000
+    hashes = [(0, 4, nb), (0, 6, nb)] if kind == "bp2ht" else [(0, 4, nb), (0, 6, nb), (0, 9, nb)]
+    cfg = bht.craft_config(kind, nb, b, hashes, threshold=12, max_chain=3)
+    table = bht.HashTable(cfg, 0)
+    table.set_blocked_insert(3)
+    keys = np.arange(1, n + 1, dtype=np.uint32)
+    o = table.insert(dev(keys), dev(keys ^ np.uint32(0x5A5A)))
+    room = b * len(hashes)
+    assert o.inserted == room and o.failed == n - room, o
+    assert table.occupied_slots() == room
+    s = table.download_store().reshape(nb, b)
+    used = np.flatnonzero((s != np.uint64(0xFFFFFFFFFFFFFFFF)).any(axis=1))
+    assert used.tolist() == sorted({h[1] for h in hashes})
+    k = (s[used] & np.uint64(0xFFFFFFFF)).astype(np.uint32).ravel()
+    v = (s[used] >> np.uint64(32)).astype(np.uint32).ravel()
+    assert np.unique(k).size == room and np.array_equal(v, k ^ np.uint32(0x5A5A))
+    o2 = table.insert(dev(keys + np.uint32(n)), dev(keys))
+    assert o2.inserted == 0 and o2.failed == n and table.occupied_slots() == room
+    # ordinary keys still land next to the hot buckets: a fresh uniform config on the same handle size
+    cfg2 = bht.make_config(kind, 300_000, 0.8, b, seed=5)
+    t2 = bht.HashTable(cfg2, 0)
+    t2.set_blocked_insert(3)
+    uk = unique_keys(300_000, 77)
+    o3 = t2.insert(dev(uk), dev(uk))
+    assert o3.success and np.array_equal(host(t2.find(dev(uk))), uk)
+
+
 @pytest.mark.parametrize("kind,b,lf", [("bp2ht", 16, 0.8), ("iht", 16, 0.8), ("bp2ht", 32, 0.85)])
 def test_stability_placed_pairs_never_move(bht, kind, b, lf):
     # test_table.cpp:262-284, acceptance.cpp:392-422
