@@ -143,7 +143,9 @@ int32_t bht_device_of(const bht_table* table);
  * (table.cpp:203-212) with explicit values.  Precondition as in the reference: keys unique,
  * != sentinel, not yet present.  Unlike the reference's build, which stops at the first failed
  * key, every pair is attempted; pairs that do not fit are reported in `result`, not as an error.
- * `result` may be NULL (no synchronisation; fetch it later with bht_last_insert_result). */
+ * `result` may be NULL (no synchronisation; fetch it later with bht_last_insert_result).
+ * `values` may be NULL: every key is paired with value_for_key(key) as in the reference's keys-only build
+ * (table.cpp:234, keygen.hpp:23-26); the values are made on the device, so a BHT_MEM_HOST caller ships keys only. */
 bht_status bht_insert(bht_table* table, const uint32_t* keys, const uint32_t* values, uint64_t n,
                       int32_t mem_space, bht_insert_result* result, void* stream);
 
@@ -155,7 +157,8 @@ bht_status bht_find(const bht_table* table, const uint32_t* keys, uint32_t* out_
 
 /* build(keys, cfg, opts) (table.hpp:125-127, table.cpp:224-276) in one call: BHT_CAPACITY_EXCEEDED when
  * n > cfg->capacity ("build: key set exceeds table capacity", table.cpp:225, checked before anything is
- * allocated), else bht_create + bht_insert of all n pairs.  *out receives the new table. */
+ * allocated), else bht_create + bht_insert of all n pairs.  *out receives the new table.  values == NULL is the
+ * reference's signature: build(keys, cfg, opts) pairs key k with value_for_key(k). */
 bht_status bht_build(const bht_config* cfg, int32_t device, const uint32_t* keys, const uint32_t* values,
                      uint64_t n, int32_t mem_space, int32_t iht_prose_fallback, bht_table** out,
                      bht_insert_result* result, void* stream);
@@ -191,8 +194,11 @@ bht_status bht_set_iht_prose_fallback(bht_table* table, int32_t enabled);
  * kernel.  1cht, and bcht tables beyond 8 GB: the pairs are routed by L2-sized region and inserted by the general
  * kernel in that order.  mode 0 = never (caller order), 1 = when the sizes make it pay (default), 2 = always the
  * L2-routed build, 3 = always the shared-memory-blocked build (2 and 3 also on small tables; used by the parity
- * tests).  bp2ht / iht are never blocked: their balanced placements depend on the arrival order, and arrival in
- * first-bucket order measurably lowers the load factor they reach. */
+ * tests).  bp2ht / iht are never reordered: their balanced placements depend on the arrival order, and arrival in
+ * first-bucket order measurably lowers the load factor they reach.  For them the mode selects how loads are learnt:
+ * modes 1 (stores of 192 MB and more) and 3 (always) decide from a per-bucket load counter array kept beside the
+ * store and claim slots with an atomic on the counter — one 8-byte store per pair is the only access to the store;
+ * mode 0 reads the candidate buckets.  Same decisions, same probe counts, in the caller's order either way. */
 bht_status bht_set_blocked_insert(bht_table* table, int32_t mode);
 
 /* cuckoo kinds, off by default: insert the pairs that arrive beyond load 0.98 (b = 1: 0.85) with few keys in flight

@@ -247,12 +247,11 @@ class hash_table {
 inline std::pair<hash_table, build_outcome> build(const key_type* keys, std::uint64_t n, const table_config& cfg,
                                                   build_options opts = {}) {
   if (n > cfg.capacity) throw std::invalid_argument("build: key set exceeds table capacity");
-  if (opts.space != mem_space::host) throw std::invalid_argument("build: derives values on the host; pass host keys or use build_pairs()");
-  std::vector<value_type> values(n);
-  for (std::uint64_t i = 0; i < n; ++i) values[i] = value_for_key(keys[i]);
   bht_table* h = nullptr;
   bht_insert_result r{};
-  check(bht_build(&cfg, opts.device, keys, values.data(), n, BHT_MEM_HOST, opts.iht_prose_fallback ? 1 : 0, &h, &r, opts.stream));
+  // NULL values: the library pairs every key with value_for_key(key) on the device (keys in either memory space)
+  check(bht_build(&cfg, opts.device, keys, nullptr, n, static_cast<std::int32_t>(opts.space), opts.iht_prose_fallback ? 1 : 0, &h, &r,
+                  opts.stream));
   return {hash_table(h, cfg), hash_table::outcome_of(r)};
 }
 

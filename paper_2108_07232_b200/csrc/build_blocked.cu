@@ -120,9 +120,15 @@ group_scatter_kernel(const __grid_constant__ HashFn h0, uint32_t region_log2, ui
 #pragma unroll
     for (int j = 0; j < kGroups; ++j) {
       const uint64_t i = i0 + (static_cast<uint64_t>(j) * kSplitBlock + threadIdx.x) * 4;
-      const uint4 k4 = load_group4(keys, i, n, aligned), v4 = load_group4(values, i, n, aligned);
+      const uint4 k4 = load_group4(keys, i, n, aligned);
       k[j][0] = k4.x, k[j][1] = k4.y, k[j][2] = k4.z, k[j][3] = k4.w;
-      v[j][0] = v4.x, v[j][1] = v4.y, v[j][2] = v4.z, v[j][3] = v4.w;
+      if (values != nullptr) {
+        const uint4 v4 = load_group4(values, i, n, aligned);
+        v[j][0] = v4.x, v[j][1] = v4.y, v[j][2] = v4.z, v[j][3] = v4.w;
+      } else {  // keys-only build: the value is value_for_key(key) (table.cpp:234)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) v[j][e] = value_for_key(k[j][e]);
+      }
     }
 #pragma unroll
     for (int j = 0; j < kGroups; ++j) {
@@ -478,7 +484,7 @@ cudaError_t launch_blocked_build(const TableView& t, const BlockedPlan& p, const
   cudaError_t e = cudaMemsetAsync(spill_cursor, 0, 16 + (static_cast<size_t>(p.n_regions) + p.n_groups) * 4, stream);
   if (e != cudaSuccess) return e;
 
-  const bool aligned = ((reinterpret_cast<uintptr_t>(keys) | reinterpret_cast<uintptr_t>(values)) & 15) == 0;
+  const bool aligned = ((reinterpret_cast<uintptr_t>(keys) | reinterpret_cast<uintptr_t>(values)) & 15) == 0;  // values may be null
   const uint32_t inv_per = static_cast<uint32_t>((1ull << 32) / p.per) + 1u;  // exact quotient for fine ids < 2^16, per <= 256
   const uint64_t tiles_a = (n + kSplitTile - 1) / kSplitTile;
   const int grid_a = static_cast<int>(std::min<uint64_t>(tiles_a, static_cast<uint64_t>(sm_count) * 8));

@@ -384,11 +384,20 @@ bool kind_matches(int32_t table_kind, int32_t as_kind) {
 bht_status do_insert(bht_table* t, const uint32_t* keys, const uint32_t* values, uint64_t n, int32_t mem_space,
                      bht_insert_result* result, void* stream_v) {
   if (t == nullptr) return fail(BHT_INVALID_ARGUMENT, "bht_insert: null table");
-  if (n != 0 && (keys == nullptr || values == nullptr)) return fail(BHT_INVALID_ARGUMENT, "bht_insert: null keys / values");
+  if (n != 0 && keys == nullptr) return fail(BHT_INVALID_ARGUMENT, "bht_insert: null keys");
   if (mem_space != BHT_MEM_DEVICE && mem_space != BHT_MEM_HOST) return fail(BHT_INVALID_ARGUMENT, "bht_insert: bad mem_space");
   BHT_ON_DEVICE(t->device);
   std::lock_guard<std::mutex> lock(t->mu);
   cudaStream_t stream = as_stream(stream_v);
+  // values == NULL: the keys-only build of the reference, every key paired with value_for_key(key) (table.cpp:234).
+  // Host callers then ship keys only; the values are made on the device.
+  const bool derive = values == nullptr;
+  struct AsyncBuffer {  // stream-ordered scratch, released on every exit path
+    void* p = nullptr;
+    cudaStream_t s = nullptr;
+    ~AsyncBuffer() { if (p != nullptr) cudaFreeAsync(p, s); }
+  } derived;
+  derived.s = stream;
 
   BHT_CUDA(cudaMemsetAsync(t->ctr, 0, kPerCallCounterBytes, stream));
   const TailPlan tail = tail_plan(t, n);
@@ -398,6 +407,13 @@ bht_status do_insert(bht_table* t, const uint32_t* keys, const uint32_t* values,
     BHT_CUDA(cudaEventRecord(t->phase_ev[0], stream));
     const BlockedPlan plan = smem_blocked_plan(t, n);
     const uint32_t regions = plan.n_regions != 0 ? 1 : blocked_regions(t, n);
+    if (derive && n_all != 0 && (plan.n_regions == 0 || tail.tail != 0)) {
+      // the shared-memory-blocked build makes the values in its first pass; every other schedule reads an array
+      BHT_CUDA(cudaMallocAsync(&derived.p, n_all * sizeof(uint32_t), stream));
+      BHT_CUDA(launch_derive_values(keys, static_cast<uint32_t*>(derived.p), n_all, t->sm_count, stream));
+      if (plan.n_regions == 0) values = static_cast<const uint32_t*>(derived.p);
+    }
+    const uint32_t* tail_values = derive ? static_cast<const uint32_t*>(derived.p) : values;
     if (plan.n_regions != 0) {
       // Shared-memory-blocked build (build_blocked.cu): bin the pairs by the shared-memory-sized table region of
       // their first bucket, build every region in shared memory, then run the general kernel over the pairs whose
@@ -432,7 +448,7 @@ bht_status do_insert(bht_table* t, const uint32_t* keys, const uint32_t* values,
       BHT_CUDA(launch_insert_kind(t, PairSource{keys, values}, n, 0, stream));
     }
     if (tail.tail != 0)
-      BHT_CUDA(launch_insert_kind(t, PairSource{keys + n, values + n}, tail.tail, 0, stream, false, nullptr, tail.grid));
+      BHT_CUDA(launch_insert_kind(t, PairSource{keys + n, tail_values + n}, tail.tail, 0, stream, false, nullptr, tail.grid));
     BHT_CUDA(cudaEventRecord(t->phase_ev[2], stream));
     t->phases_recorded = true;
   } else if (n_all != 0) {
@@ -452,9 +468,10 @@ bht_status do_insert(bht_table* t, const uint32_t* keys, const uint32_t* values,
       chunks = c + 1;
       if (c >= kStageSlots) BHT_CUDA(cudaStreamWaitEvent(st.h2d, st.kernel_done[slot], 0));
       BHT_CUDA(cudaMemcpyAsync(st.keys[slot], keys + off, len * sizeof(uint32_t), cudaMemcpyHostToDevice, st.h2d));
-      BHT_CUDA(cudaMemcpyAsync(st.vals[slot], values + off, len * sizeof(uint32_t), cudaMemcpyHostToDevice, st.h2d));
+      if (!derive) BHT_CUDA(cudaMemcpyAsync(st.vals[slot], values + off, len * sizeof(uint32_t), cudaMemcpyHostToDevice, st.h2d));
       BHT_CUDA(cudaEventRecord(st.in_done[slot], st.h2d));
       BHT_CUDA(cudaStreamWaitEvent(st.compute, st.in_done[slot], 0));
+      if (derive) BHT_CUDA(launch_derive_values(st.keys[slot], st.vals[slot], len, t->sm_count, st.compute));
       BHT_CUDA(launch_insert_kind(t, PairSource{st.keys[slot], st.vals[slot]}, len, 0, st.compute, false, nullptr,
                                   off >= n_main ? tail.grid : 0));
       BHT_CUDA(cudaEventRecord(st.kernel_done[slot], st.compute));

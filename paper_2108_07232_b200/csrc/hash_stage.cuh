@@ -116,6 +116,11 @@ __host__ __device__ __forceinline__ uint32_t unique_key(uint32_t k0, uint32_t k1
   if (y == kEmptyKey) y = mix32(k0, k1, y);  // the sentinel is no fixed point unless nothing maps to it
   return y;
 }
+// value_for_key (reference: proj/include/bht/keygen.hpp:23-26): the value build() pairs with a key (table.cpp:234).
+__host__ __device__ __forceinline__ uint32_t value_for_key(uint32_t key) {
+  const uint32_t v = key ^ 0x5A5A5A5Au;
+  return v == kEmptyKey ? (v & 0x7FFFFFFFu) : v;
+}
 // A value stream independent of the key bijection, never the sentinel.
 __host__ __device__ __forceinline__ uint32_t synthetic_value(uint32_t k1, uint32_t key) {
   const uint32_t v = mix32(k1 ^ 0x9E3779B9u, 0x7F4A7C15u, key);

@@ -78,6 +78,8 @@ cudaError_t launch_count_occupied(const uint64_t* store, uint64_t n_slots, unsig
 cudaError_t launch_count_inadmissible(const TableView& t, unsigned long long* out, int sm_count, cudaStream_t stream);
 cudaError_t launch_hash_keys(const HashFn& h, const uint32_t* keys, uint32_t* out, uint64_t n, int sm_count,
                              cudaStream_t stream);
+// values[i] = value_for_key(keys[i]): the pairing of a keys-only build (table.cpp:234)
+cudaError_t launch_derive_values(const uint32_t* keys, uint32_t* values, uint64_t n, int sm_count, cudaStream_t stream);
 constexpr int kMaxShards = 256;
 // counts / cursors: n_dest device words each; scratch8: n bytes (4-byte aligned) for the per-key destinations.
 // out_* receive the elements grouped by destination.

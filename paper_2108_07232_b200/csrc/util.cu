@@ -119,6 +119,29 @@ cudaError_t launch_hash_keys(const HashFn& h, const uint32_t* keys, uint32_t* ou
   return cudaGetLastError();
 }
 
+// ---- values of a keys-only build: values[i] = value_for_key(keys[i]) (table.cpp:234) ------------------------------
+__global__ void __launch_bounds__(kStreamBlock)
+derive_values_kernel(const uint32_t* __restrict__ keys, uint32_t* __restrict__ values, uint64_t n, bool aligned) {
+  const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t i = tid * 4; i < n; i += stride * 4) {
+    if (aligned && i + 4 <= n) {
+      const uint4 k = *reinterpret_cast<const uint4*>(keys + i);
+      *reinterpret_cast<uint4*>(values + i) = make_uint4(value_for_key(k.x), value_for_key(k.y), value_for_key(k.z), value_for_key(k.w));
+    } else {
+      for (uint64_t j = i; j < n && j < i + 4; ++j) values[j] = value_for_key(keys[j]);
+    }
+  }
+}
+
+cudaError_t launch_derive_values(const uint32_t* keys, uint32_t* values, uint64_t n, int sm_count, cudaStream_t stream) {
+  if (n == 0) return cudaSuccess;
+  const bool aligned = ((reinterpret_cast<uintptr_t>(keys) | reinterpret_cast<uintptr_t>(values)) & 15) == 0;
+  derive_values_kernel<<<stream_grid(sm_count, n, kStreamBlock * 4), kStreamBlock, 0, stream>>>(keys, values, n, aligned);
+  note_launch();
+  return cudaGetLastError();
+}
+
 // ---- K8: routing by owner shard (multi-GPU) or by table region (L2-blocked build) ------------------
 // Pass 1 hashes every key once: it writes the destination of each key as one byte (dest8, n bytes of scratch)
 // and builds the per-destination histogram in per-thread private shared-memory counters (no atomics, no bank

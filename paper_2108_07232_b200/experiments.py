@@ -261,7 +261,7 @@ def run_trial(cell: TrialCell, device: int = 0) -> TrialOutcome:
     if keys is None or keys.size() != cell.n:
         keys = workload.generate_keys(mix_seed(cell.seed, 0x6B657973), cell.n, device=device)
     d_keys = _device_keys(keys, device)
-    d_vals = values_for_keys(d_keys)  # build() pairs every key with value_for_key (table.cpp:234)
+    d_vals = None  # keys-only build: the library pairs every key with value_for_key (table.cpp:234) on the device
 
     ins_probes = ins_ops = 0
     ins_seconds = 0.0
@@ -335,7 +335,7 @@ def run_success_rate(params: KindParams, n: int, lf_grid: Sequence[float], succe
     result = SuccessRateResult()
     keys = workload.generate_keys(mix_seed(seed, 0x6B657973), n, device=device)
     d_keys = _device_keys(keys, device)
-    d_vals = values_for_keys(d_keys)
+    d_vals = None  # keys-only build (table.cpp:234)
     for cell, lf in enumerate(lf_grid):
         point = SuccessRatePoint(lf=lf, trials=success_trials)
         table = None

@@ -298,7 +298,9 @@ class HashTable:
     def set_blocked_insert(self, mode) -> None:
         """Blocked builds of device-resident inserts: 0 / False = never (caller order), 1 / True = when the sizes
         make it pay (default: shared-memory-blocked for bcht, L2-routed for 1cht), 2 = always the L2-routed build,
-        3 = always the shared-memory-blocked build.  bp2ht / iht always insert in caller order."""
+        3 = always the shared-memory-blocked build.  bp2ht / iht always insert in caller order; for them modes 1 (stores
+        of 192 MB and more) and 3 take the loads from the per-bucket counter array (csrc/insert_claim.cu), mode 0 reads
+        the candidate buckets."""
         _check(self._lib.bht_set_blocked_insert(self._h, int(mode)))
 
     # -- the hot path
@@ -309,10 +311,11 @@ class HashTable:
         ``values=None`` derives value_for_key(k) as ``build`` does (table.cpp:234).  ``as_kind`` selects the
         reference's per-variant entry point (bcht_insert / bp2ht_insert / iht_insert) and its kind check.
         """
-        if values is None:
-            values = values_for_keys(keys)
         kp, kn, kspace, _k = _as_u32(keys, "keys")
-        vp, vn, vspace, _v = _as_u32(values, "values")
+        if values is None:  # NULL values: the library pairs every key with value_for_key(key) on the device
+            vp, vn, vspace, _v = None, kn, kspace, None
+        else:
+            vp, vn, vspace, _v = _as_u32(values, "values")
         if kspace != vspace:
             raise ValueError("insert: keys and values must live in the same memory space")
         n = kn if n is None else int(n)
@@ -436,10 +439,11 @@ def build(keys, cfg: Config, values=None, device: Optional[int] = None, iht_pros
     Unlike the reference, which stops at the first failed key, every key is attempted; ``success`` still means
     inserted == len(keys).  Raises CapacityError when len(keys) > capacity, before touching the device store.
     """
-    if values is None:
-        values = values_for_keys(keys)
     kp, kn, kspace, _k = _as_u32(keys, "keys")
-    vp, vn, vspace, _v = _as_u32(values, "values")
+    if values is None:  # the reference's signature: the library pairs key k with value_for_key(k) on the device
+        vp, vn, vspace, _v = None, kn, kspace, None
+    else:
+        vp, vn, vspace, _v = _as_u32(values, "values")
     if kspace != vspace or kn != vn:
         raise ValueError("build: keys and values must have the same length and memory space")
     if device is None:

@@ -196,6 +196,37 @@ def test_build_parity_routed(bht, ora, monkeypatch, kind, b, lf, t, mode):
             assert table.occupied_slots() == n + 2000 and table.count_inadmissible() == 0
 
 
+@pytest.mark.parametrize("kind,b,lf,mode", [("bcht", 16, 0.9, 3), ("bcht", 16, 0.9, 2), ("bcht", 8, 0.85, 0), ("1cht", 1, 0.7, 1),
+                                            ("bp2ht", 16, 0.75, 3), ("bp2ht", 16, 0.75, 0), ("iht", 16, 0.8, 3), ("iht", 32, 0.8, 0)])
+@pytest.mark.parametrize("space", ["device", "host"])
+def test_keys_only_insert_pairs_every_key_with_value_for_key(bht, ora, kind, b, lf, mode, space):
+    """values = NULL through the C ABI: build(keys, cfg) pairs key k with value_for_key(k) (table.cpp:234, keygen.hpp:23-26).
+    Same stored multiset and answers as the explicit-values call, for every schedule, from device and from host memory,
+    in one batch and in ragged batches (and with the throttled tail, which reads the derived array at an offset)."""
+    n = 180_001
+    keys = unique_keys(n, 900 + b)
+    keys[5] = np.uint32(0xFFFFFFFF ^ 0x5A5A5A5A)  # the one key whose image would be the sentinel (keygen.hpp:25)
+    keys = np.unique(keys)
+    np.random.Generator(np.random.MT19937(3)).shuffle(keys)
+    n = keys.size
+    want_vals = ora.values_for_keys(keys)
+    assert want_vals[np.flatnonzero(keys == np.uint32(0xFFFFFFFF ^ 0x5A5A5A5A))[0]] == np.uint32(0x7FFFFFFF)
+    extra = {"threshold": int(0.8 * b)} if kind == "iht" else {}
+    cfg = bht.make_config(kind, n, lf, b, seed=bht.mix_seed(5, b), **extra)
+    src = dev(keys) if space == "device" else keys
+    for cuts, throttle in [((0, n), False), ((0, 1, 70_003, n), True)]:
+        table = bht.HashTable(cfg, 0)
+        table.set_blocked_insert(mode)
+        table.set_tail_throttle(throttle)
+        ok = True
+        for lo, hi in zip(cuts[:-1], cuts[1:]):
+            ok &= table.insert(src[lo:hi]).success
+        assert ok and table.occupied_slots() == n and table.count_inadmissible() == 0
+        assert np.array_equal(stored_pairs(table.download_store()), packed(keys, want_vals))
+        assert np.array_equal(host(table.find(dev(keys))), want_vals)
+        table.close()
+
+
 def test_build_default_values_and_host_memory(bht, ora):
     """values=None -> value_for_key (table.cpp:234); host arrays go through the staged PCIe path."""
     n = 300_000

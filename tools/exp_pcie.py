@@ -35,3 +35,11 @@ def ins_nores(): table.clear(); table.insert(hk, hv, want_result=False)
 def fnd(): table.find(hk, ho)
 print(f"host insert (with result): {t(ins)*1e3:.2f} ms; without result {t(ins_nores)*1e3:.2f} ms; host find {t(fnd)*1e3:.2f} ms; floor = {(0.4/ (0.4/h2d) + 0.2/(0.4/h2d))*1e3:.2f} ms")
 assert torch.equal(ho, hv)
+# keys-only build (values = NULL -> value_for_key on the device): half the H2D bytes of the insert
+want = bht.values_for_keys(k.view(torch.int32)).view(torch.int32).cpu()
+def ins_keys(): table.clear(); table.insert(hk)
+def ins_keys_nores(): table.clear(); table.insert(hk, want_result=False)
+def both_legs(): table.clear(); table.insert(hk); table.find(hk, ho)
+print(f"keys-only host insert (with result): {t(ins_keys)*1e3:.2f} ms; without result {t(ins_keys_nores)*1e3:.2f} ms; "
+      f"insert + find {t(both_legs)*1e3:.2f} ms; floor = {(0.2 / (0.4/h2d) + 0.2/(0.4/h2d))*1e3:.2f} ms")
+assert torch.equal(ho, want)
