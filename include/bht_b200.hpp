@@ -22,7 +22,9 @@
 #define BHT_B200_HPP_
 
 #include <cstdint>
+#include <chrono>
 #include <cstdio>
+#include <ostream>
 #include <optional>
 #include <stdexcept>
 #include <string>
@@ -338,6 +340,8 @@ struct trial_outcome {
   double realized_lf = 0.0;
   double insert_mean_probes = 0.0;
   std::vector<double> find_mean_probes;  // parallel to the requested ratios
+  double insert_ops_per_sec = 0.0;       // steady_clock around the bulk calls (the reference times build(), table.cpp:228-276)
+  std::vector<double> find_ops_per_sec;
 };
 
 // run_trial: fresh hash constants per attempt (mix_seed(seed, 0x100 + attempt)), build until `trials` successes or the
@@ -345,6 +349,10 @@ struct trial_outcome {
 inline trial_outcome run_trial(const trial_cell& cell) {
   trial_outcome out;
   out.find_mean_probes.assign(cell.positive_ratios.size(), 0.0);
+  out.find_ops_per_sec.assign(cell.positive_ratios.size(), 0.0);
+  using clock = std::chrono::steady_clock;
+  double ins_seconds = 0.0;
+  std::vector<double> find_seconds(cell.positive_ratios.size(), 0.0);
   key_set local;
   const key_set* keys = cell.preloaded_keys;
   if (keys == nullptr || keys->size() != cell.n) {
@@ -361,7 +369,9 @@ inline trial_outcome run_trial(const trial_cell& cell) {
                                    mix_seed(cell.seed, 0x100 + attempt), cell.max_chain);
     ++attempt;
     out.realized_lf = static_cast<double>(cell.n) / static_cast<double>(cfg.capacity);
+    const auto t_build = clock::now();
     auto [table, built] = build(keys->keys.data(), cell.n, cfg, cell.build_opts);
+    const double build_seconds = std::chrono::duration<double>(clock::now() - t_build).count();
     if (!built.success) {
       ++out.failures;
       continue;
@@ -369,6 +379,7 @@ inline trial_outcome run_trial(const trial_cell& cell) {
     ++out.successes;
     ins_probes += built.probes;
     ins_ops += built.attempted;
+    ins_seconds += build_seconds;
     for (std::size_t r = 0; r < cell.positive_ratios.size(); ++r) {
       if (queries[r].empty() && cell.n != 0) {
         for (const query& qu : generate_queries(*keys, cell.positive_ratios[r], cell.n, mix_seed(cell.seed, 0x200 + r),
@@ -376,15 +387,20 @@ inline trial_outcome run_trial(const trial_cell& cell) {
           queries[r].push_back(qu.key);
       }
       find_stats fs;
+      const auto t_find = clock::now();
       table.find(queries[r].data(), answers.data(), cell.n, mem_space::host, nullptr, &fs);
+      find_seconds[r] += std::chrono::duration<double>(clock::now() - t_find).count();
       find_probes[r] += fs.probes;
       find_ops[r] += fs.queries;
     }
   }
   out.budget_exhausted = out.successes < cell.trials;
   out.insert_mean_probes = ins_ops ? static_cast<double>(ins_probes) / static_cast<double>(ins_ops) : 0.0;
-  for (std::size_t r = 0; r < cell.positive_ratios.size(); ++r)
+  out.insert_ops_per_sec = ins_seconds > 0.0 ? static_cast<double>(ins_ops) / ins_seconds : 0.0;
+  for (std::size_t r = 0; r < cell.positive_ratios.size(); ++r) {
     out.find_mean_probes[r] = find_ops[r] ? static_cast<double>(find_probes[r]) / static_cast<double>(find_ops[r]) : 0.0;
+    out.find_ops_per_sec[r] = find_seconds[r] > 0.0 ? static_cast<double>(find_ops[r]) / find_seconds[r] : 0.0;
+  }
   return out;
 }
 
@@ -466,6 +482,93 @@ inline std::string csv_line(const result_record& r) {
   s += ',' + format_double(r.mean_probes) + ',' + format_double(r.ops_per_sec) + ',' + std::to_string(r.successes) + ',' +
        std::to_string(r.failures) + ',' + std::to_string(r.seed);
   return s;
+}
+
+// experiment_spec / run_experiment / write_csv (experiments.hpp:28-113, experiments.cpp:153-243): the grid driver above
+// run_trial and run_success_rate — same cell order, same cell seeds (cell_seed(seed, running cell index)), one record per
+// (cell, op, positive ratio); success-rate scenarios give one "build" record per load factor.
+enum class scenario { probe_analysis, throughput, success_rate };
+struct experiment_spec {
+  scenario scen = scenario::probe_analysis;
+  std::vector<kind_params> kinds;
+  std::vector<std::uint64_t> n_grid;
+  std::vector<double> lf_grid;
+  std::vector<double> positive_ratios;
+  unsigned trials = 10;
+  unsigned max_failures = 50;
+  unsigned success_trials = 200;
+  std::uint64_t seed = 0;
+  build_options build_opts;
+  std::optional<std::uint32_t> max_chain;
+};
+struct experiment_result {
+  std::vector<result_record> records;
+  double wall_seconds = 0.0;
+  bool any_budget_exhausted() const {
+    for (const auto& r : records)
+      if (r.budget_exhausted) return true;
+    return false;
+  }
+};
+
+inline experiment_result run_experiment(const experiment_spec& spec) {
+  if (spec.kinds.empty()) throw std::invalid_argument("run_experiment: no table kinds requested");
+  if (spec.n_grid.empty()) throw std::invalid_argument("run_experiment: empty key-count grid");
+  if (spec.lf_grid.empty()) throw std::invalid_argument("run_experiment: empty load-factor grid");
+  if (spec.trials < 1) throw std::invalid_argument("run_experiment: trials must be at least 1");
+  experiment_result result;
+  const auto start = std::chrono::steady_clock::now();
+  std::uint64_t cell_index = 0;
+  for (const kind_params& params : spec.kinds) {
+    std::optional<std::uint32_t> tpct;
+    if (params.kind == table_kind::iht) tpct = params.threshold_pct;
+    auto record = [&](std::uint64_t n, double realized, const char* op) {
+      result_record r;
+      r.kind = params.kind; r.b = params.bucket_size; r.threshold_pct = tpct; r.n = n; r.realized_lf = realized; r.op = op;
+      r.seed = spec.seed;
+      return r;
+    };
+    for (std::uint64_t n : spec.n_grid) {
+      if (spec.scen == scenario::success_rate) {
+        build_options opts = spec.build_opts;
+        const success_rate_result sr = run_success_rate(params, n, spec.lf_grid, spec.success_trials, mix_seed(spec.seed, cell_index),
+                                                        spec.max_chain, opts);
+        ++cell_index;
+        for (const success_rate_point& p : sr.points) {
+          result_record r = record(n, p.realized_lf, "build");
+          r.successes = p.successes;
+          r.failures = p.trials - p.successes;
+          result.records.push_back(r);
+        }
+        continue;
+      }
+      for (double lf : spec.lf_grid) {
+        trial_cell cell;
+        cell.params = params; cell.n = n; cell.lf = lf; cell.positive_ratios = spec.positive_ratios; cell.trials = spec.trials;
+        cell.max_failures = spec.max_failures; cell.seed = cell_seed(spec.seed, cell_index); cell.build_opts = spec.build_opts;
+        cell.max_chain = spec.max_chain;
+        ++cell_index;
+        const trial_outcome o = run_trial(cell);
+        result_record ins = record(n, o.realized_lf, "insert");
+        ins.mean_probes = o.insert_mean_probes; ins.ops_per_sec = o.insert_ops_per_sec; ins.successes = o.successes;
+        ins.failures = o.failures; ins.budget_exhausted = o.budget_exhausted;
+        result.records.push_back(ins);
+        for (std::size_t r = 0; r < spec.positive_ratios.size(); ++r) {
+          result_record f = record(n, o.realized_lf, "find");
+          f.positive_ratio = spec.positive_ratios[r]; f.mean_probes = o.find_mean_probes[r]; f.ops_per_sec = o.find_ops_per_sec[r];
+          f.successes = o.successes; f.failures = o.failures; f.budget_exhausted = o.budget_exhausted;
+          result.records.push_back(f);
+        }
+      }
+    }
+  }
+  result.wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - start).count();
+  return result;
+}
+
+inline void write_csv(std::ostream& out, const experiment_result& result) {
+  out << result_csv_header << '\n';
+  for (const result_record& r : result.records) out << csv_line(r) << '\n';
 }
 
 }  // namespace gpu

@@ -1,10 +1,13 @@
 // C++ caller of include/bht_b200.hpp, written the way a caller of the reference's table.hpp is written
 // (proj/tests/test_table.cpp shapes): build, bulk find, per-key find_key, error behaviour.  Exit code 0 = all checks pass.
 // With the argument "nogpu" only the host-side checks run (used by the CPU test tier).
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <random>
 #include <unordered_set>
+#include <sstream>
+#include <algorithm>
 #include <vector>
 
 #include "bht_b200.hpp"
@@ -158,6 +161,54 @@ int main(int argc, char** argv) {
     rec.kind = table_kind::bcht; rec.threshold_pct.reset(); rec.op = "insert"; rec.positive_ratio.reset(); rec.mean_probes = 1.10823;
     CHECK(csv_line(rec) == "bcht,16,,3000,0.797872,insert,,1.10823,1.5e+07,2,0,42");
     CHECK(std::string(result_csv_header) == "kind,b,threshold_pct,n,realized_lf,op,positive_ratio,mean_probes,ops_per_sec,successes,failures,seed");
+  }
+  // run_experiment / write_csv (test_experiments.cpp:140-190): record order, cell seeds, CSV shape
+  {
+    experiment_spec spec;
+    spec.kinds = {{table_kind::bcht, 16, 80}, {table_kind::iht, 16, 75}};
+    spec.n_grid = {4000};
+    spec.lf_grid = {0.1, 0.5};
+    spec.positive_ratios = {1.0, 0.0};
+    spec.trials = 2;
+    spec.seed = 42;
+    experiment_result res = run_experiment(spec);
+    CHECK(res.records.size() == 12 && !res.any_budget_exhausted() && res.wall_seconds > 0.0);
+    for (std::size_t i = 0; i < res.records.size(); ++i) {
+      const result_record& r = res.records[i];
+      const bool iht = i >= 6;
+      CHECK(r.kind == (iht ? table_kind::iht : table_kind::bcht) && r.b == 16 && r.n == 4000 && r.seed == 42);
+      CHECK(r.threshold_pct.has_value() == iht && (!iht || *r.threshold_pct == 75));
+      CHECK(r.successes == 2 && r.failures == 0 && r.ops_per_sec > 0.0);
+      CHECK(r.op == (i % 3 == 0 ? "insert" : "find"));
+      CHECK(r.positive_ratio.has_value() == (i % 3 != 0));
+      if (i % 3 == 1) CHECK(*r.positive_ratio == 1.0);
+      if (i % 3 == 2) CHECK(*r.positive_ratio == 0.0);
+      if (!iht && i < 3) CHECK(r.mean_probes == 1.0);           // bcht at load factor 0.1: one probe, whatever the op
+      if (iht && i % 3 == 2) CHECK(r.mean_probes == 3.0);       // iht negative queries read all three buckets
+      if (iht && i % 3 == 1) CHECK(r.mean_probes >= 1.0 && r.mean_probes < 1.5);
+    }
+    CHECK(res.records[0].realized_lf < res.records[3].realized_lf);  // lf grid order inside a kind
+    // the same cell through run_trial directly: same seed derivation -> same table geometry, same probe means (up to the
+    // order in which concurrent claims land)
+    trial_cell cell;
+    cell.params = spec.kinds[1]; cell.n = 4000; cell.lf = 0.5; cell.positive_ratios = spec.positive_ratios; cell.trials = 2;
+    cell.seed = cell_seed(42, 3);
+    trial_outcome o = run_trial(cell);
+    CHECK(std::fabs(o.find_mean_probes[0] - res.records[10].mean_probes) < 0.02 && o.realized_lf == res.records[9].realized_lf);
+    std::ostringstream csv;
+    write_csv(csv, res);
+    const std::string text = csv.str();
+    CHECK(text.rfind(std::string(result_csv_header) + "\n", 0) == 0);
+    CHECK(static_cast<std::size_t>(std::count(text.begin(), text.end(), '\n')) == 13);
+    CHECK(text.find("\niht,16,75,4000,") != std::string::npos && text.find("\nbcht,16,,4000,") != std::string::npos);
+    spec.scen = scenario::success_rate;
+    spec.lf_grid = {0.01, 0.5};
+    spec.success_trials = 5;
+    experiment_result sr = run_experiment(spec);
+    CHECK(sr.records.size() == 4);
+    for (const result_record& r : sr.records) CHECK(r.op == "build" && r.successes == 5 && r.failures == 0 && !r.positive_ratio);
+    experiment_spec bad;
+    CHECK(throws<std::invalid_argument>([&] { run_experiment(bad); }));
   }
   // set_blocked_insert is part of the handle API (host batches are always staged in caller order; the device-resident
   // schedules are covered by tests/test_gpu_parity.py::test_build_parity_routed)
