@@ -282,6 +282,27 @@ bht_status bht_load_keys(const char* path, uint32_t* keys_host, uint64_t max_key
 uint32_t bht_unique_key_host(uint64_t seed, uint32_t counter);
 uint32_t bht_synthetic_value_host(uint64_t seed, uint32_t key);
 
+/* ---- sharded table handle: one process, n_shards ordinary tables, one per entry of device_ids ----------------
+ * (the multi-process counterpart, one rank per GPU over NCCL, is paper_2108_07232_b200/sharded.py).
+ * owner(k) = bht_shard_of_host(alpha, beta, n_shards, k) with (alpha, beta) = bht_shard_constants(cfg->seed), so every
+ * candidate bucket of a key lives in one shard.  keys[g] / values[g] / out_values[g] are DEVICE pointers on
+ * device_ids[g] holding the slice of n[g] elements that GPU g contributes; the routed runs travel with
+ * cudaMemcpyPeerAsync (NVLink where peer access exists) and all owners insert / find at the same time.  Device ids
+ * may repeat (several shards on one GPU).  values == NULL or values[g] == NULL: value_for_key, as in bht_insert.
+ * `result` aggregates the shards (attempted = total keys; success = every pair placed); may be NULL. */
+typedef struct bht_sharded bht_sharded;
+void bht_shard_constants(uint64_t seed, uint64_t* alpha, uint64_t* beta);
+bht_status bht_sharded_create(const bht_config* cfg_per_shard, uint32_t n_shards, const int32_t* device_ids, bht_sharded** out);
+bht_status bht_sharded_destroy(bht_sharded* sharded);
+uint32_t bht_sharded_count(const bht_sharded* sharded);
+/* the table of one shard, owned by the sharded handle (for bht_load_factor, bht_download_store, ...) */
+bht_status bht_sharded_table(bht_sharded* sharded, uint32_t shard, bht_table** out);
+bht_status bht_sharded_clear(bht_sharded* sharded);
+bht_status bht_sharded_insert(bht_sharded* sharded, const uint32_t* const* keys, const uint32_t* const* values,
+                              const uint64_t* n, bht_insert_result* result);
+bht_status bht_sharded_find(bht_sharded* sharded, const uint32_t* const* keys, uint32_t* const* out_values,
+                            const uint64_t* n, bht_find_result* result);
+
 /* ---- pinned host buffers for BHT_MEM_HOST callers (cudaMallocHost / cudaFreeHost) --------- */
 
 bht_status bht_host_alloc(size_t bytes, void** out);

@@ -484,6 +484,42 @@ inline std::string csv_line(const result_record& r) {
   return s;
 }
 
+// The single-process sharded handle (bht_sharded_*, csrc/sharded.cu): n shards, one ordinary table per device id (ids may
+// repeat); per-GPU device slices in, aggregated outcome out.  No reference counterpart.
+class sharded_table {
+ public:
+  sharded_table(const table_config& cfg_per_shard, const std::vector<std::int32_t>& device_ids) : cfg_(cfg_per_shard) {
+    check(bht_sharded_create(&cfg_, static_cast<std::uint32_t>(device_ids.size()), device_ids.data(), &h_));
+  }
+  ~sharded_table() { bht_sharded_destroy(h_); }
+  sharded_table(const sharded_table&) = delete;
+  sharded_table& operator=(const sharded_table&) = delete;
+  std::uint32_t shards() const { return bht_sharded_count(h_); }
+  bht_table* shard_handle(std::uint32_t g) {
+    bht_table* t = nullptr;
+    check(bht_sharded_table(h_, g, &t));
+    return t;
+  }
+  void clear() { check(bht_sharded_clear(h_)); }
+  // keys[g] / values[g]: device arrays of n[g] elements on the g-th device; values empty = value_for_key
+  build_outcome insert(const std::vector<const key_type*>& keys, const std::vector<const value_type*>& values,
+                       const std::vector<std::uint64_t>& n) {
+    bht_insert_result r{};
+    check(bht_sharded_insert(h_, keys.data(), values.empty() ? nullptr : values.data(), n.data(), &r));
+    return hash_table::outcome_of(r);
+  }
+  void find(const std::vector<const key_type*>& keys, const std::vector<value_type*>& out, const std::vector<std::uint64_t>& n,
+            find_stats* stats = nullptr) {
+    bht_find_result r{};
+    check(bht_sharded_find(h_, keys.data(), out.data(), n.data(), stats ? &r : nullptr));
+    if (stats) *stats = find_stats{r.queries, r.hits, r.probes, r.value_sum};
+  }
+
+ private:
+  table_config cfg_;
+  bht_sharded* h_ = nullptr;
+};
+
 // experiment_spec / run_experiment / write_csv (experiments.hpp:28-113, experiments.cpp:153-243): the grid driver above
 // run_trial and run_success_rate — same cell order, same cell seeds (cell_seed(seed, running cell index)), one record per
 // (cell, op, positive ratio); success-rate scenarios give one "build" record per load factor.

@@ -119,6 +119,14 @@ SIGNATURES = {
     "bht_shard_of_host": (C.c_uint32, [C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint32]),
     "bht_shard_partition": (C.c_int, [C.c_uint64, C.c_uint64, C.c_uint32, _vp, _vp, C.c_uint64, _vp, _vp, _vp, _u64p, C.c_int32, _vp]),
     "bht_shard_unpermute": (C.c_int, [_vp, _vp, C.c_uint64, _vp, C.c_int32, _vp]),
+    "bht_shard_constants": (None, [C.c_uint64, _u64p, _u64p]),
+    "bht_sharded_create": (C.c_int, [C.POINTER(Config), C.c_uint32, C.POINTER(C.c_int32), C.POINTER(_vp)]),
+    "bht_sharded_destroy": (C.c_int, [_vp]),
+    "bht_sharded_count": (C.c_uint32, [_vp]),
+    "bht_sharded_table": (C.c_int, [_vp, C.c_uint32, C.POINTER(_vp)]),
+    "bht_sharded_clear": (C.c_int, [_vp]),
+    "bht_sharded_insert": (C.c_int, [_vp, C.POINTER(_vp), C.POINTER(_vp), _u64p, C.POINTER(InsertResult)]),
+    "bht_sharded_find": (C.c_int, [_vp, C.POINTER(_vp), C.POINTER(_vp), _u64p, C.POINTER(FindResult)]),
     "bht_generate_unique_keys": (C.c_int, [C.c_uint64, C.c_uint64, C.c_uint64, _vp, _vp, C.c_int32, _vp]),
     "bht_unique_key_host": (C.c_uint32, [C.c_uint64, C.c_uint32]),
     "bht_synthetic_value_host": (C.c_uint32, [C.c_uint64, C.c_uint32]),

@@ -221,3 +221,86 @@ class ShardedTable:
 
     def realized_load(self) -> float:
         return self.inserted() / (self.cfg.capacity * self.world)
+
+
+class LocalShardedTable:
+    """The single-process sharded handle of the C ABI (``bht_sharded_*``, csrc/sharded.cu): ``len(device_ids)`` shards,
+    one ordinary table per entry (ids may repeat), routed by the same constants as :class:`ShardedTable`.  ``insert`` /
+    ``find`` take one device tensor per shard — the slice that GPU contributes — and move the routed runs with peer
+    copies; all owners work at the same time."""
+
+    def __init__(self, cfg_per_shard, device_ids: Sequence[int]):
+        self._lib = _lib.load()
+        self.cfg = cfg_per_shard
+        self.device_ids = [int(d) for d in device_ids]
+        self._h = C.c_void_p()
+        ids = (C.c_int32 * len(self.device_ids))(*self.device_ids)
+        _check(self._lib.bht_sharded_create(C.byref(cfg_per_shard), len(self.device_ids), ids, C.byref(self._h)))
+        a, b = C.c_uint64(), C.c_uint64()
+        self._lib.bht_shard_constants(cfg_per_shard.seed, C.byref(a), C.byref(b))
+        self.alpha, self.beta = a.value, b.value
+
+    def close(self) -> None:
+        if getattr(self, "_h", None) is not None and self._h:
+            self._lib.bht_sharded_destroy(self._h)
+            self._h = C.c_void_p()
+
+    __del__ = close
+
+    def __len__(self) -> int:
+        return self._lib.bht_sharded_count(self._h)
+
+    def shard(self, g: int) -> HashTable:
+        """The table of shard g, borrowed (owned by this handle)."""
+        h = C.c_void_p()
+        _check(self._lib.bht_sharded_table(self._h, g, C.byref(h)))
+        return HashTable._borrow(h, self.cfg, self.device_ids[g])
+
+    def clear(self) -> None:
+        _check(self._lib.bht_sharded_clear(self._h))
+
+    def _slices(self, tensors, what: str):
+        if len(tensors) != len(self.device_ids):
+            raise ValueError(f"{what}: one tensor per shard expected")
+        ptrs = (C.c_void_p * len(tensors))()
+        ns = (C.c_uint64 * len(tensors))()
+        for g, t in enumerate(tensors):
+            if t is None:
+                ptrs[g], ns[g] = None, 0
+                continue
+            if not (isinstance(t, torch.Tensor) and t.is_cuda and t.device.index == self.device_ids[g]):
+                raise ValueError(f"{what}[{g}]: a tensor on cuda:{self.device_ids[g]} expected")
+            if t.dtype not in (torch.int32, torch.uint32) or t.dim() != 1 or not t.is_contiguous():
+                raise ValueError(f"{what}[{g}]: 1-D contiguous int32 / uint32 tensor expected")
+            ptrs[g], ns[g] = t.data_ptr(), t.numel()
+        return ptrs, ns
+
+    def insert(self, keys: Sequence[torch.Tensor], values: Optional[Sequence[Optional[torch.Tensor]]] = None) -> BuildOutcome:
+        for t in keys:
+            if t is not None:
+                torch.cuda.current_stream(t.device).synchronize()  # the handle works on its own streams
+        kp, ns = self._slices(keys, "keys")
+        vp = None
+        if values is not None:
+            vp, vns = self._slices(values, "values")
+            for g in range(len(ns)):
+                if values[g] is not None and vns[g] != ns[g]:
+                    raise ValueError("insert: keys and values of a shard must have the same length")
+        res = _lib.InsertResult()
+        _check(self._lib.bht_sharded_insert(self._h, kp, vp, ns, C.byref(res)))
+        return BuildOutcome(bool(res.success), res.inserted, res.failed, res.attempted, res.probes,
+                            None if res.first_failed_key == _lib.EMPTY_KEY else res.first_failed_key)
+
+    def find(self, keys: Sequence[torch.Tensor], want_stats: bool = False):
+        for t in keys:
+            if t is not None:
+                torch.cuda.current_stream(t.device).synchronize()
+        kp, ns = self._slices(keys, "keys")
+        outs = [None if t is None else torch.empty_like(t) for t in keys]
+        op, _ = self._slices(outs, "out")
+        res = _lib.FindResult()
+        _check(self._lib.bht_sharded_find(self._h, kp, op, ns, C.byref(res) if want_stats else None))
+        if want_stats:
+            from .table import FindStats
+            return outs, FindStats(res.queries, res.hits, res.probes, res.value_sum)
+        return outs

@@ -231,10 +231,18 @@ class HashTable:
         self._cfg = cfg.copy()
         return self
 
+    @classmethod
+    def _borrow(cls, handle, cfg: Config, device: int) -> "HashTable":
+        """Wraps a table owned by someone else (a shard of bht_sharded): close() does not destroy it."""
+        self = cls._adopt(handle, cfg, device)
+        self._borrowed = True
+        return self
+
     # -- lifetime
     def close(self) -> None:
         if getattr(self, "_h", None) is not None and self._h:
-            self._lib.bht_destroy(self._h)
+            if not getattr(self, "_borrowed", False):
+                self._lib.bht_destroy(self._h)
             self._h = C.c_void_p()
 
     def __del__(self):
