@@ -396,6 +396,8 @@ def run_cuda(args):
         roofline["kernel"] = dom_kernel
         roofline["algorithmic_bytes_per_key"] = dom_bytes / n
         roofline["frac_of_8TBps"] = dom_bytes / (dom_ms * 1e-3) / 8e12
+        # the stricter variant: the sector model plus the streamed arrays (find: 4 B key in + 4 B value out; insert: 8 B in)
+        roofline["frac_with_streaming_io"] = (dom_bytes + 8 * n) / (dom_ms * 1e-3) / 1e9 / peaks["hbm_gbs"]
         roofline["note"] = ("achieved = sector-model bytes (probes x 4 sectors, + 1 written sector per inserted pair, x 32 B) / "
                             "this kernel's CUDA-event time; traffic = its ncu dram bytes per launch (L2 hits make it smaller "
                             "than the model). detail.roofline_insert_op is the whole bulk insert (partition passes, "
