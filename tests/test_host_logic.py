@@ -195,3 +195,15 @@ def test_product_never_imports_the_oracle():
         path = os.path.join(ROOT, "tools", f)
         if os.path.isfile(path) and f.endswith(".py"):
             assert "from oracle" not in open(path).read() and "import oracle" not in open(path).read(), path
+
+
+def test_shard_constants_same_in_c_and_python(bht):
+    """bht_shard_constants (csrc/sharded.cu) and sharded.shard_constants derive the routing hash of the sharded table
+    the same way, so the single-process handle and the one-rank-per-GPU table build the same shards."""
+    lib = bht._lib.load()
+    rng = np.random.default_rng(11)
+    for seed in [0, 1, 2, 0x73686172, (1 << 64) - 1] + [int(x) for x in rng.integers(0, 1 << 63, size=50)]:
+        a, b = C.c_uint64(), C.c_uint64()
+        lib.bht_shard_constants(seed, C.byref(a), C.byref(b))
+        assert (a.value, b.value) == tuple(bht.shard_constants(seed))
+        assert 1 <= a.value < 4294967291 and b.value < 4294967291
