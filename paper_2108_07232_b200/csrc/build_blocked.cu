@@ -18,7 +18,9 @@
 //   K11 region_build    one CTA per fine region: the region's buckets live in shared memory (filled with the empty
 //                       pattern when the table is known to be empty, else loaded from the store), every pair of the
 //                       bin claims slot = atomicAdd(load counter of its bucket) — a shared-memory atomic, no CAS, no
-//                       lost races, no re-probes — and the region is written back with coalesced 16-byte stores.
+//                       lost races, no re-probes — and the region is written back by the bulk-copy engine
+//                       (cp.async.bulk shared -> global, SASS UBLKCP, 4 KiB pieces: 0.771 -> 0.746 ms for the three
+//                       passes against coalesced 16-byte stores from registers).
 //                       A pair whose bucket is full goes to a per-CTA stash; once every claim is written the stashed
 //                       pairs do their first eviction in shared memory (atomicExch into a random slot of the full
 //                       bucket, table.cpp:67-81) and the VICTIMS go to the global spill list, each with the bucket
@@ -46,6 +48,10 @@
 #ifndef BHT_BUILD_BLOCK  // measured (insert, 50 M pairs): 192 x 20: 1.087 ms, 256 x 16: 1.062, 320 x 12: 1.034, 384 x 10: 1.034 (spills)
 #define BHT_BUILD_BLOCK 320
 #define BHT_BUILD_U 12
+#endif
+
+#ifndef BHT_BUILD_TMA_STORE
+#define BHT_BUILD_TMA_STORE 1
 #endif
 
 namespace bht_b200 {
@@ -403,14 +409,31 @@ region_build_kernel(const __grid_constant__ TableView t, uint32_t region_log2, u
       sp.start[stash_base + i] = next | 0x80000000u;
     }
   }
+#if BHT_BUILD_TMA_STORE
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // this thread's shared-memory writes, for the bulk-copy engine
+#endif
   __syncthreads();
 
-  // phase 2: the region back to the store, coalesced
+  // phase 2: the region back to the store
   {
+#if BHT_BUILD_TMA_STORE
+    // bulk asynchronous copies shared -> global (cp.async.bulk, the TMA unit): 4 KiB pieces issued by the first threads,
+    // no register staging and no load/store-unit traffic for the 64 KiB of the region
+    constexpr uint32_t kPiece = 4096;
+    const uint32_t bulk_bytes = (n_slots << 3) & ~15u;
+    const uint32_t rows_saddr = static_cast<uint32_t>(__cvta_generic_to_shared(rows));
+    unsigned char* gbytes = reinterpret_cast<unsigned char*>(gstore);
+    for (uint32_t p = threadIdx.x * kPiece; p < bulk_bytes; p += kBuildBlock * kPiece) {
+      const uint32_t sz = min(kPiece, bulk_bytes - p);
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gbytes + p), "r"(rows_saddr + p), "r"(sz) : "memory");
+    }
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+#else
     const uint4* rows4 = reinterpret_cast<const uint4*>(rows);
     uint4* g4 = reinterpret_cast<uint4*>(gstore);
     const uint32_t n4 = n_slots >> 1;
     for (uint32_t i = threadIdx.x; i < n4; i += kBuildBlock) g4[i] = rows4[i];
+#endif
     if ((n_slots & 1u) && threadIdx.x == 0) gstore[n_slots - 1] = rows[n_slots - 1];
     if (threadIdx.x == 0 && (placed_count != 0 || stashed != 0)) {
       const unsigned long long a = static_cast<unsigned long long>(placed_count) + hole_count;
@@ -420,6 +443,9 @@ region_build_kernel(const __grid_constant__ TableView t, uint32_t region_log2, u
       }
       atomicAdd(&ctr->insert_probes, static_cast<unsigned long long>(placed_count) + stashed);
     }
+#if BHT_BUILD_TMA_STORE
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // shared memory may go once the copies have read it
+#endif
   }
 }
 
