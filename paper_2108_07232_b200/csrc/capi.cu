@@ -109,6 +109,10 @@ struct bht_table {
   // build, 3 = always the shared-memory-blocked build (bcht, 8 <= b <= 32; else as 2); bp2ht / iht are never blocked
   int blocked_insert = 1;
   bool known_empty = true;  // no slot has been written since create / clear: a blocked build need not read the store
+  // The fill of create / clear is deferred until something reads or partially writes the store: a shared-memory-blocked
+  // build into an empty table writes every region of the store exactly once, empty slots included (K11), so the fill
+  // is fused into it; every other use of the store calls materialize_clear first.
+  std::atomic<bool> clear_pending{false};
   uint64_t host_inserted = 0;  // upper bound of the pairs in the store, kept on the host (tail_plan)
   bool tail_throttle = false;  // bht_set_tail_throttle
   // bp2ht / iht: one 32-bit load counter per bucket for the counter-claimed insert (insert_claim.cu); loads_valid =
@@ -374,6 +378,14 @@ TailPlan tail_plan(const bht_table* t, uint64_t n) {
   return p;
 }
 
+// Writes the empty pattern a deferred create / clear still owes (caller holds t->mu, or is the only user of t).
+cudaError_t materialize_clear(bht_table* t, cudaStream_t stream) {
+  if (!t->clear_pending.load(std::memory_order_acquire)) return cudaSuccess;
+  const cudaError_t e = launch_fill_empty(t->view.store, t->cfg.capacity, t->sm_count, stream);
+  if (e == cudaSuccess) t->clear_pending.store(false, std::memory_order_release);
+  return e;
+}
+
 bool kind_matches(int32_t table_kind, int32_t as_kind) {
   // bcht_insert / bcht_find accept both cuckoo kinds (table.cpp:55,96)
   const bool cuckoo = table_kind == BHT_ONE_CHT || table_kind == BHT_BCHT;
@@ -407,6 +419,10 @@ bht_status do_insert(bht_table* t, const uint32_t* keys, const uint32_t* values,
     BHT_CUDA(cudaEventRecord(t->phase_ev[0], stream));
     const BlockedPlan plan = smem_blocked_plan(t, n);
     const uint32_t regions = plan.n_regions != 0 ? 1 : blocked_regions(t, n);
+    if (plan.n_regions != 0 && t->known_empty && n != 0)
+      t->clear_pending.store(false, std::memory_order_release);  // the region build writes every slot of the store
+    else
+      BHT_CUDA(materialize_clear(t, stream));
     if (derive && n_all != 0 && (plan.n_regions == 0 || tail.tail != 0)) {
       // the shared-memory-blocked build makes the values in its first pass; every other schedule reads an array
       BHT_CUDA(cudaMallocAsync(&derived.p, n_all * sizeof(uint32_t), stream));
@@ -456,6 +472,7 @@ bht_status do_insert(bht_table* t, const uint32_t* keys, const uint32_t* values,
     const uint64_t n_main = n_all - tail.tail;
     bht_status s = ensure_staging(t);
     if (s != BHT_OK) return s;
+    BHT_CUDA(materialize_clear(t, stream));
     Staging& st = t->stage;
     cudaEvent_t start = st.out_done[0];  // reuse as the "counters are zeroed" marker
     BHT_CUDA(cudaEventRecord(start, stream));
@@ -500,6 +517,10 @@ bht_status do_find(const bht_table* ct, bool early_exit, const uint32_t* keys, u
   BHT_ON_DEVICE(t->device);
   cudaStream_t stream = as_stream(stream_v);
 
+  if (t->clear_pending.load(std::memory_order_acquire)) {
+    std::lock_guard<std::mutex> lock(t->mu);
+    BHT_CUDA(materialize_clear(t, stream));
+  }
   if (mem_space == BHT_MEM_DEVICE && result == nullptr) {
     // lock-free: concurrent finds on different streams share nothing but the read-only store
     uint32_t* cursor = nullptr;
@@ -685,7 +706,7 @@ bht_status bht_create(const bht_config* cfg, int32_t device, bht_table** out) {
     t->loads_valid = e == cudaSuccess;
   }
   if (e == cudaSuccess) e = cudaMemset(t->ctr, 0, sizeof(DevCounters));
-  if (e == cudaSuccess) e = launch_fill_empty(store, cfg->capacity, t->sm_count, nullptr);
+  t->clear_pending.store(true);  // the store is filled by its first user (materialize_clear) or by a blocked build
   if (e == cudaSuccess) e = cudaStreamSynchronize(nullptr);
   if (e != cudaSuccess) {
     if (store) cudaFree(store);
@@ -739,7 +760,7 @@ bht_status bht_clear(bht_table* t, void* stream) {
   if (t == nullptr) return fail(BHT_INVALID_ARGUMENT, "bht_clear: null table");
   BHT_ON_DEVICE(t->device);
   std::lock_guard<std::mutex> lock(t->mu);
-  BHT_CUDA(launch_fill_empty(t->view.store, t->cfg.capacity, t->sm_count, as_stream(stream)));
+  t->clear_pending.store(true, std::memory_order_release);  // deferred, see bht_table::clear_pending
   BHT_CUDA(cudaMemsetAsync(t->ctr, 0, sizeof(DevCounters), as_stream(stream)));
   t->known_empty = true;
   t->host_inserted = 0;
@@ -886,6 +907,7 @@ bht_status bht_count_occupied(const bht_table* ct, uint64_t* occupied, void* str
   bht_table* t = const_cast<bht_table*>(ct);
   BHT_ON_DEVICE(t->device);
   std::lock_guard<std::mutex> lock(t->mu);
+  BHT_CUDA(materialize_clear(t, as_stream(stream)));
   BHT_CUDA(launch_count_occupied(t->view.store, t->cfg.capacity, &t->ctr->scratch, t->sm_count, as_stream(stream)));
   bht_status s = read_counters(t, as_stream(stream));
   if (s != BHT_OK) return s;
@@ -898,6 +920,7 @@ bht_status bht_count_inadmissible(const bht_table* ct, uint64_t* violations, voi
   bht_table* t = const_cast<bht_table*>(ct);
   BHT_ON_DEVICE(t->device);
   std::lock_guard<std::mutex> lock(t->mu);
+  BHT_CUDA(materialize_clear(t, as_stream(stream)));
   BHT_CUDA(launch_count_inadmissible(t->view, &t->ctr->scratch, t->sm_count, as_stream(stream)));
   bht_status s = read_counters(t, as_stream(stream));
   if (s != BHT_OK) return s;
@@ -908,6 +931,11 @@ bht_status bht_count_inadmissible(const bht_table* ct, uint64_t* violations, voi
 bht_status bht_download_store(const bht_table* t, uint64_t* host_dst, void* stream) {
   if (t == nullptr || host_dst == nullptr) return fail(BHT_INVALID_ARGUMENT, "bht_download_store: null argument");
   BHT_ON_DEVICE(t->device);
+  {
+    bht_table* mt = const_cast<bht_table*>(t);
+    std::lock_guard<std::mutex> lock(mt->mu);
+    BHT_CUDA(materialize_clear(mt, as_stream(stream)));
+  }
   BHT_CUDA(cudaMemcpyAsync(host_dst, t->view.store, t->cfg.capacity * sizeof(uint64_t), cudaMemcpyDeviceToHost,
                            as_stream(stream)));
   BHT_CUDA(cudaStreamSynchronize(as_stream(stream)));
@@ -921,6 +949,7 @@ bht_status bht_upload_store(bht_table* t, const uint64_t* host_src, void* stream
   cudaStream_t s = as_stream(stream);
   t->known_empty = false;
   t->loads_valid = false;
+  t->clear_pending.store(false, std::memory_order_release);  // every slot is overwritten
   BHT_CUDA(cudaMemcpyAsync(t->view.store, host_src, t->cfg.capacity * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
   BHT_CUDA(cudaMemsetAsync(t->ctr, 0, sizeof(DevCounters), s));
   BHT_CUDA(launch_count_occupied(t->view.store, t->cfg.capacity, &t->ctr->inserted_total, t->sm_count, s));
@@ -954,8 +983,19 @@ bht_status bht_dump_store(const bht_table* t, const char* path) {
 
 uint64_t* bht_device_store(const bht_table* t) {
   if (t == nullptr) return nullptr;
-  const_cast<bht_table*>(t)->known_empty = false;  // the caller may write slots behind the library's back
-  const_cast<bht_table*>(t)->loads_valid = false;
+  bht_table* mt = const_cast<bht_table*>(t);
+  {
+    std::lock_guard<std::mutex> lock(mt->mu);
+    if (mt->clear_pending.load()) {  // the caller gets a store that is what the API said it was, whatever stream it uses next
+      int prev = 0;
+      cudaGetDevice(&prev);
+      cudaSetDevice(mt->device);
+      if (materialize_clear(mt, nullptr) == cudaSuccess) cudaStreamSynchronize(nullptr);
+      cudaSetDevice(prev);
+    }
+  }
+  mt->known_empty = false;  // the caller may write slots behind the library's back
+  mt->loads_valid = false;
   return t->view.store;
 }
 

@@ -311,3 +311,40 @@ def test_blocked_build_with_skewed_first_buckets(bht, ora, b, skew_regions):
     assert table2.occupied_slots() == o1.inserted + o2.inserted and table2.count_inadmissible() == 0
     if o1.success and o2.success:
         assert np.array_equal(host(table2.find(dev(keys))), values)
+
+
+@pytest.mark.parametrize("mode", [0, 3])
+def test_deferred_clear_is_indistinguishable_from_a_fill(bht, mode):
+    """bht_create / bht_clear defer the fill of the store (csrc/capi.cu, clear_pending): a shared-memory-blocked build into
+    the empty table writes every region once, empty slots included, and every other use fills first.  Whatever follows a
+    clear must see an empty table, and nothing of the previous contents may survive a clear + build."""
+    n = 150_001
+    a, b_keys = unique_keys(2 * n, 321)[:n], unique_keys(2 * n, 321)[n:]
+    cfg = bht.make_config("bcht", n, 0.85, 16, seed=4)
+    table = bht.HashTable(cfg, 0)                       # created, never filled yet
+    assert table.occupied_slots() == 0
+    table = bht.HashTable(cfg, 0)
+    assert np.all(host(table.find(dev(a[:1000]))) == EMPTY)
+    table = bht.HashTable(cfg, 0)
+    assert np.all(table.download_store() == np.uint64(0xFFFFFFFFFFFFFFFF))
+    table = bht.HashTable(cfg, 0)
+    table.set_blocked_insert(mode)
+    assert table.insert(dev(a), dev(a)).success
+    assert np.array_equal(host(table.find(dev(a))), a)
+    table.clear()
+    assert table.inserted() == 0
+    assert np.all(host(table.find(dev(a))) == EMPTY)    # find after a deferred clear
+    assert table.insert(dev(a), dev(a)).success
+    table.clear()
+    m = n // 3
+    assert table.insert(dev(b_keys[:m]), dev(b_keys[:m])).success   # clear + build: the build writes the whole store
+    assert table.occupied_slots() == m and table.count_inadmissible() == 0
+    assert np.all(host(table.find(dev(a))) == EMPTY)
+    assert np.array_equal(host(table.find(dev(b_keys[:m]))), b_keys[:m])
+    table.clear()
+    table.clear()
+    assert table.occupied_slots() == 0
+    assert int((table.device_store() != -1).sum().item()) == 0   # the zero-copy view is filled before it is handed out
+    # a small (unblocked) batch right after a clear
+    assert table.insert(dev(a[:100]), dev(a[:100])).success
+    assert table.occupied_slots() == 100 and np.array_equal(host(table.find(dev(a[:100]))), a[:100])
