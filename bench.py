@@ -405,6 +405,8 @@ def run_cuda(args):
                             "than the random-sector model charges, so its fraction exceeds 1")
         detail = {
             "clear_ms": clear_ms, "insert_ms": ins_ms, "find_ms": find_ms,
+            "clear_note": "bht_clear defers the fill; the blocked build's region write-back (K11) writes every slot of the store "
+                          "once, empty ones included, so the step has no separate fill pass (DESIGN.md, Deferred fill)",
             "insert_blocked_build_ms": ins_prepare_ms, "insert_walk_kernel_ms": ins_kernel_ms,
             "insert_keys_only_ms": ins_keys_only_ms, "insert_keys_only_mkeys": n / (ins_keys_only_ms * 1e-3) / 1e6,
             "insert_mkeys": n / ins_ms / 1e3, "find_100_mkeys": n / find_ms / 1e3,
