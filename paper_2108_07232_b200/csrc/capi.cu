@@ -378,6 +378,16 @@ TailPlan tail_plan(const bht_table* t, uint64_t n) {
   return p;
 }
 
+// Deferring the fill pays when the next build is likely to be the shared-memory-blocked one (which writes every slot
+// itself): bcht tables beyond the L2 in the default mode, any cuckoo table when that build is forced.  Everything else
+// is filled at once, so that no later call pays for it.
+bool defer_fill_pays(const bht_table* t) {
+  const bool cuckoo = t->cfg.kind == BHT_BCHT || t->cfg.kind == BHT_ONE_CHT;
+  if (!cuckoo || t->blocked_insert == 0 || t->blocked_insert == 2) return false;
+  if (t->blocked_insert == 3) return true;
+  return t->cfg.kind == BHT_BCHT && t->cfg.capacity * sizeof(uint64_t) >= (192ull << 20);
+}
+
 // Writes the empty pattern a deferred create / clear still owes (caller holds t->mu, or is the only user of t).
 cudaError_t materialize_clear(bht_table* t, cudaStream_t stream) {
   if (!t->clear_pending.load(std::memory_order_acquire)) return cudaSuccess;
@@ -706,7 +716,9 @@ bht_status bht_create(const bht_config* cfg, int32_t device, bht_table** out) {
     t->loads_valid = e == cudaSuccess;
   }
   if (e == cudaSuccess) e = cudaMemset(t->ctr, 0, sizeof(DevCounters));
-  t->clear_pending.store(true);  // the store is filled by its first user (materialize_clear) or by a blocked build
+  t->cfg = *cfg;
+  if (defer_fill_pays(t)) t->clear_pending.store(true);  // filled by its first user (materialize_clear) or by a blocked build
+  else if (e == cudaSuccess) e = launch_fill_empty(store, cfg->capacity, t->sm_count, nullptr);
   if (e == cudaSuccess) e = cudaStreamSynchronize(nullptr);
   if (e != cudaSuccess) {
     if (store) cudaFree(store);
@@ -760,7 +772,12 @@ bht_status bht_clear(bht_table* t, void* stream) {
   if (t == nullptr) return fail(BHT_INVALID_ARGUMENT, "bht_clear: null table");
   BHT_ON_DEVICE(t->device);
   std::lock_guard<std::mutex> lock(t->mu);
-  t->clear_pending.store(true, std::memory_order_release);  // deferred, see bht_table::clear_pending
+  if (defer_fill_pays(t)) {
+    t->clear_pending.store(true, std::memory_order_release);  // deferred, see bht_table::clear_pending
+  } else {
+    BHT_CUDA(launch_fill_empty(t->view.store, t->cfg.capacity, t->sm_count, as_stream(stream)));
+    t->clear_pending.store(false, std::memory_order_release);
+  }
   BHT_CUDA(cudaMemsetAsync(t->ctr, 0, sizeof(DevCounters), as_stream(stream)));
   t->known_empty = true;
   t->host_inserted = 0;
