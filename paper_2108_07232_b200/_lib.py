@@ -9,7 +9,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libbht_b200.so")
+# BHT_B200_LIB: another build of the same library (A/B runs of tuning macros, csrc/Makefile VARIANT=...)
+LIB_PATH = os.environ.get("BHT_B200_LIB") or os.path.join(HERE, "lib", "libbht_b200.so")
 
 OK, INVALID_ARGUMENT, KIND_MISMATCH, CAPACITY_EXCEEDED, CUDA_ERROR, COMM_ERROR, IO_ERROR = range(7)
 MEM_DEVICE, MEM_HOST = 0, 1

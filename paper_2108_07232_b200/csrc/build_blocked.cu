@@ -1,4 +1,4 @@
-// build_blocked.cu — K10 / K11: the shared-memory-blocked bulk build of the cuckoo tables (bcht, 1cht).
+// build_blocked.cu — K8g / K10 / K11: the shared-memory-blocked bulk build of the cuckoo tables (bcht, 1cht).
 //
 // Same algorithm as bcht_insert (reference: proj/src/table.cpp:53-92) — a pair goes to slot index = load of its
 // H0 bucket (table.cpp:85); when that bucket is full the insertion goes on as an eviction chain (table.cpp:63-81)
@@ -21,10 +21,10 @@
 //                       lost races, no re-probes — and the region is written back by the bulk-copy engine
 //                       (cp.async.bulk shared -> global, SASS UBLKCP, 4 KiB pieces: 0.771 -> 0.746 ms for the three
 //                       passes against coalesced 16-byte stores from registers).
-//                       A pair whose bucket is full goes to a per-CTA stash; once every claim is written the stashed
-//                       pairs do their first eviction in shared memory (atomicExch into a random slot of the full
-//                       bucket, table.cpp:67-81) and the VICTIMS go to the global spill list, each with the bucket
-//                       its walk goes on in and a chain length of 1 (one list reservation per CTA).
+//                       A pair whose bucket is full leaves its bin position in a per-CTA stash; once every claim is
+//                       written the stashed pairs do their first eviction in shared memory (atomicExch into a random
+//                       slot of the full bucket, table.cpp:67-81) and the VICTIMS go to the global spill list, each
+//                       with the bucket its walk goes on in and a chain length of 1 (one list reservation per CTA).
 //   K4  (existing)      the general cuckoo kernel (insert_cuckoo.cu) finishes the walks of the spill list exactly as
 //                       the reference would: probe the next bucket, claim or evict again, up to max_chain.
 //
@@ -54,18 +54,25 @@
 #define BHT_BUILD_TMA_STORE 1
 #endif
 
+#ifndef BHT_SPLIT_TMA  // 1: the next tile's input arrives by a bulk asynchronous copy (TMA) while this one is processed
+#define BHT_SPLIT_TMA 1
+#endif
+#ifndef BHT_SPLIT_CTAS  // resident CTAs per SM the partition kernels are compiled for (register budget)
+#define BHT_SPLIT_CTAS (BHT_SPLIT_TMA ? 4 : 5)
+#endif
+#ifndef BHT_SPLIT_BLOCK
+#define BHT_SPLIT_BLOCK 256
+#endif
+
 namespace bht_b200 {
 
 namespace {
 
-constexpr int kSplitBlock = 256;
-#ifndef BHT_SPLIT_PER_THREAD
-#define BHT_SPLIT_PER_THREAD 8
-#endif
-constexpr int kSplitPerThread = BHT_SPLIT_PER_THREAD;
+constexpr int kSplitBlock = BHT_SPLIT_BLOCK;  // >= 256: the first 256 threads scan the tile's histogram
+constexpr int kSplitPerThread = 8;
 constexpr int kSplitTile = kSplitBlock * kSplitPerThread;  // 2048 pairs
 constexpr int kBuildBlock = BHT_BUILD_BLOCK;   // few threads with many loads in flight each: 3 CTAs/SM by shared memory
-constexpr uint32_t kStashPairs = 1024;  // per-CTA stash of spilled pairs (K11)
+constexpr uint32_t kStashPairs = 4096;  // per-CTA stash of spilled pairs (K11): 16-bit positions in the region's bin
 constexpr uint32_t kRegionBytesLog2 = 16;
 
 // The spill list: packed pairs + where their walk starts (kStartAtH0 for a pair that has not probed anything yet).
@@ -75,232 +82,377 @@ struct Spill {
   unsigned long long* cursor;
 };
 
-// Appends the pairs of the lanes with `spilled` to the spill list as fresh pairs: one global atomic per warp (rare paths).
-__device__ __forceinline__ void spill_append(bool spilled, uint2 kv, const Spill& sp, int lane) {
-  uint2* __restrict__ spill = sp.pairs;
-  unsigned long long* __restrict__ spill_cursor = sp.cursor;
-  const uint32_t m = __ballot_sync(kFullMask, spilled);
-  if (m == 0) return;
-  const int leader = __ffs(m) - 1;
-  unsigned long long base = 0;
-  if (lane == leader) base = atomicAdd(spill_cursor, static_cast<unsigned long long>(__popc(m)));
-  base = __shfl_sync(kFullMask, base, leader);
-  if (spilled) {
-    const unsigned long long pos = base + __popc(m & ((1u << lane) - 1u));
-    spill[pos] = kv;
-    sp.start[pos] = kStartAtH0;
+// A pair that found no room in a fixed-capacity segment / bin / stash goes to the spill list untouched (rare: the
+// capacities are mean + 6 sigma of a uniform hash; one global atomic per pair).
+__device__ __forceinline__ void spill_fresh(uint2 kv, const Spill& sp) {
+  const unsigned long long pos = atomicAdd(sp.cursor, 1ull);
+  sp.pairs[pos] = kv;
+  sp.start[pos] = kStartAtH0;
+}
+
+// ---- the partition passes (K8g, K10) ------------------------------------------------------------------------
+// One tile = 2048 pairs, 8 per thread.  (1) every pair takes a rank among the tile's pairs of its destination with one
+// shared-memory atomicAdd; (2) the 256 counts are scanned, and one global atomicAdd per (tile, destination) reserves the
+// run in the destination's fixed-capacity segment; (3) the pairs are staged in shared memory run by run; (4) the tile
+// is written out in staging order, so that consecutive threads write consecutive pairs of a run (whole 32-byte
+// sectors except at the ends of a run).  Three block barriers per tile; the histogram is zeroed by the thread that
+// scans it.
+//
+// What bounds these passes is the shared-memory pipe (ncu, profiles/r02d_*: l1tex 65-78 % busy, short-scoreboard and
+// MIO-throttle stalls, the integer pipe half idle), not DRAM and not the instruction count: with the stores removed
+// the pass still took 200 of its 230 us, halving its instructions changed nothing, fetching the next tile's input
+// with the TMA unit while this one is processed changed nothing.  So the staging keeps nothing per pair but the pair:
+// the write-out recomputes a staged pair's destination from its key (a second hash: 14 integer instructions) instead
+// of a staged position / destination byte (one more scattered shared-memory store and one more load per pair).
+struct SplitShared {
+  uint2 pair[kSplitTile];
+  uint2 out_of[256];   // per destination of the tile: {output index of its run - first staging slot, first staging slot past what fits}
+  uint32_t toff[256];  // per destination: first staging slot of its run
+  uint32_t hist[256];
+  uint32_t warp_tot[8];
+  unsigned long long mbar;   // completion of the bulk copy into `in`
+  unsigned long long pad;
+#if BHT_SPLIT_TMA
+  uint32_t in[2 * kSplitTile];  // the next full tile: K8g keys | values, K10 packed pairs
+#endif
+};
+
+__device__ __forceinline__ void mbar_init(unsigned long long* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect(unsigned long long* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* smem_dst, const void* gmem_src, uint32_t bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(smem_dst)),
+               "l"(gmem_src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@p bra DONE_%=;\n\t"
+      "bra WAIT_%=;\n\t"
+      "DONE_%=:\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// Phases 2-4 for the tile whose pairs (kv), destinations and ranks (dr = destination | rank << 8) are in registers and
+// whose ranks are all taken (the caller's barrier); `valid` has bit j set when pair j of this thread exists, `len` =
+// pairs in the tile; dest_of(key) = the destination (< 256) of a pair of this tile.
+template <bool FULL, typename DestOf>
+__device__ __forceinline__ void split_tile_finish(SplitShared& s, const uint2 (&kv)[kSplitPerThread],
+                                                  const uint32_t (&dr)[kSplitPerThread], uint32_t valid, uint32_t len,
+                                                  uint32_t n_dest, uint32_t dest_base, uint32_t cap,
+                                                  uint32_t* __restrict__ cursor, uint2* __restrict__ out, const Spill& sp,
+                                                  uint64_t tile_id, DestOf dest_of) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t h = 0, x = 0, gbase = 0;
+  if (kSplitBlock == 256 || threadIdx.x < 256) {
+    h = s.hist[threadIdx.x];
+    s.hist[threadIdx.x] = 0;  // for the next tile: nobody touches it again before the next barrier
+    x = h;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFullMask, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) s.warp_tot[warp] = x;
+    // the reservation travels while the block meets at the barrier
+    if (h != 0 && threadIdx.x < n_dest) gbase = atomicAdd(&cursor[dest_base + threadIdx.x], h);
   }
+  __syncthreads();
+  if (kSplitBlock == 256 || threadIdx.x < 256) {
+    uint32_t before = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) before += w < warp ? s.warp_tot[w] : 0u;
+    const uint32_t first = before + x - h;
+    const uint32_t room = gbase < cap ? cap - gbase : 0u;
+    s.toff[threadIdx.x] = first;
+    s.out_of[threadIdx.x] = make_uint2((dest_base + threadIdx.x) * cap + gbase - first, first + min(h, room));
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < kSplitPerThread; ++j)
+    if (FULL || ((valid >> j) & 1u)) s.pair[s.toff[dr[j] & 255u] + (dr[j] >> 8)] = kv[j];
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < kSplitPerThread; ++j) {
+    const uint32_t slot = j * kSplitBlock + threadIdx.x;
+    if (FULL || slot < len) {
+      const uint2 p = s.pair[slot];
+      const uint2 o = s.out_of[dest_of(p.x)];  // consecutive slots share a destination: mostly a broadcast
+#if defined(BHT_EXP_NOSTORE)   // experiments only (results are wrong): what the pass costs without its stores ...
+      if (slot == 0xFFFFFFF0u) __stcs(out + o.x, p);
+#elif defined(BHT_EXP_LINEAR)  // ... and with perfectly sequential ones
+      __stcs(out + (tile_id * kSplitTile + slot), p);
+#else
+      if (slot < o.y) __stcs(out + (o.x + slot), p);
+      else spill_fresh(p, sp);  // the destination's segment is full (rare: sized mean + 6 sigma)
+#endif
+    }
+  }
+  // no barrier here: the next tile's first writes to `pair` / `toff` / `out_of` come after its own barriers
 }
 
 // ---- K8g ------------------------------------------------------------------------------------------------------
-// First partition level, one pass: every pair goes to the segment of its GROUP (= `per` consecutive fine regions).
-// Tiles of 2048 pairs are ranked by group in shared memory, one global atomicAdd per (tile, group) reserves a run in
-// the group's fixed-capacity segment, the tile is staged by group and written out run by run (~25 pairs per run).
-// No histogram pre-pass and no destination bytes: the hash is uniform, so the segments are sized mean + 6 sigma and the
-// few pairs that do not fit go to the spill list.
-__device__ __forceinline__ uint4 load_group4(const uint32_t* __restrict__ p, uint64_t i, uint64_t n, bool aligned) {
-  if (aligned && i + 4 <= n) return __ldcs(reinterpret_cast<const uint4*>(p + i));
-  uint4 r = make_uint4(0, 0, 0, 0);
-  if (i < n) r.x = p[i];
-  if (i + 1 < n) r.y = p[i + 1];
-  if (i + 2 < n) r.z = p[i + 2];
-  if (i + 3 < n) r.w = p[i + 3];
-  return r;
-}
+// First partition level, one streaming pass over (a chunk of) the caller's arrays: every pair goes to the segment of
+// its GROUP (= `per` consecutive fine regions).  No histogram pre-pass and no destination bytes: the hash is uniform,
+// so the segments are sized mean + 6 sigma and the few pairs that do not fit go to the spill list.  The cursors live
+// across launches, so a batch may arrive in several chunks (host-buffer builds, sharded builds).
+struct GroupArgs {
+  HashFn h0;
+  uint32_t region_log2, inv_per, n_groups, group_cap;
+  const uint32_t* keys;
+  const uint32_t* values;  // null: keys-only build, value = value_for_key(key) (table.cpp:234)
+  uint64_t n;
+  uint32_t* group_cursor;
+  uint2* grouped;
+  Spill sp;
+  int aligned;
+};
 
-__global__ void __launch_bounds__(kSplitBlock)
-group_scatter_kernel(const __grid_constant__ HashFn h0, uint32_t region_log2, uint32_t inv_per, uint32_t n_groups, uint32_t group_cap,
-                     const uint32_t* __restrict__ keys, const uint32_t* __restrict__ values, uint64_t n, bool aligned,
-                     uint32_t* __restrict__ group_cursor, uint2* __restrict__ grouped, const Spill sp) {
-  __shared__ uint2 s_pair[kSplitTile];
-  __shared__ uint8_t s_dest[kSplitTile];
-  __shared__ uint32_t hist[256], tile_off[256], base_of[256], warp_tot[kSplitBlock / 32];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint64_t n_tiles = (n + kSplitTile - 1) / kSplitTile;
+__global__ void __launch_bounds__(kSplitBlock, BHT_SPLIT_CTAS)
+group_scatter_kernel(const __grid_constant__ GroupArgs a) {
+  extern __shared__ __align__(16) unsigned char split_bytes[];
+  SplitShared& s = *reinterpret_cast<SplitShared*>(split_bytes);
+  if (threadIdx.x < 256) s.hist[threadIdx.x] = 0;
+  if (threadIdx.x == 0) mbar_init(&s.mbar);
+  __syncthreads();
+  const uint64_t n_tiles = (a.n + kSplitTile - 1) / kSplitTile;
+  // a full tile of 16-byte aligned arrays arrives through the bulk copy / 16-byte loads; the last, partial one (and
+  // everything of an unaligned call) is read element by element
+  auto is_full = [&](uint64_t tile) { return a.aligned && (tile + 1) * kSplitTile <= a.n; };
+  auto fetch = [&](uint64_t tile) {
+#if BHT_SPLIT_TMA
+    constexpr uint32_t in_bytes = kSplitTile * 4u;
+    if (threadIdx.x == 0 && tile < n_tiles && is_full(tile)) {
+      mbar_expect(&s.mbar, a.values != nullptr ? 2 * in_bytes : in_bytes);
+      bulk_load(s.in, a.keys + tile * kSplitTile, in_bytes, &s.mbar);
+      if (a.values != nullptr) bulk_load(s.in + kSplitTile, a.values + tile * kSplitTile, in_bytes, &s.mbar);
+    }
+#endif
+  };
+  auto group_of = [&](uint32_t key) {
+    return static_cast<uint32_t>((static_cast<uint64_t>(bucket_index(a.h0, key) >> a.region_log2) * a.inv_per) >> 32);
+  };
+  uint32_t parity = 0;
+  fetch(blockIdx.x);
   for (uint64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
     const uint64_t i0 = tile * kSplitTile;
-    hist[threadIdx.x] = 0;
-    __syncthreads();
-    constexpr int kGroups = kSplitPerThread / 4;  // groups of 4 consecutive pairs per thread
-    uint32_t k[kGroups][4], v[kGroups][4], dst[kGroups][4], rank[kGroups][4];
-#pragma unroll
-    for (int j = 0; j < kGroups; ++j) {
-      const uint64_t i = i0 + (static_cast<uint64_t>(j) * kSplitBlock + threadIdx.x) * 4;
-      const uint4 k4 = load_group4(keys, i, n, aligned);
-      k[j][0] = k4.x, k[j][1] = k4.y, k[j][2] = k4.z, k[j][3] = k4.w;
-      if (values != nullptr) {
-        const uint4 v4 = load_group4(values, i, n, aligned);
-        v[j][0] = v4.x, v[j][1] = v4.y, v[j][2] = v4.z, v[j][3] = v4.w;
-      } else {  // keys-only build: the value is value_for_key(key) (table.cpp:234)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) v[j][e] = value_for_key(k[j][e]);
-      }
+    const bool full = is_full(tile);  // block-uniform
+    const uint32_t len = static_cast<uint32_t>(min(static_cast<uint64_t>(kSplitTile), a.n - i0));
+    uint2 kv[kSplitPerThread];
+    uint32_t dr[kSplitPerThread];
+    uint32_t valid = 0;
+#if BHT_SPLIT_TMA
+    if (full) {
+      mbar_wait(&s.mbar, parity);
+      parity ^= 1u;
     }
+#endif
 #pragma unroll
-    for (int j = 0; j < kGroups; ++j) {
-      const uint64_t i = i0 + (static_cast<uint64_t>(j) * kSplitBlock + threadIdx.x) * 4;
+    for (int j = 0; j < kSplitPerThread / 4; ++j) {
+      const uint32_t at = (j * kSplitBlock + threadIdx.x) * 4;  // this thread's four consecutive pairs
+      uint32_t k[4], v[4] = {0u, 0u, 0u, 0u};
+      if (full) {
+#if BHT_SPLIT_TMA
+        const uint4 k4 = *reinterpret_cast<const uint4*>(s.in + at);
+#else
+        const uint4 k4 = __ldcs(reinterpret_cast<const uint4*>(a.keys + i0 + at));
+#endif
+        k[0] = k4.x, k[1] = k4.y, k[2] = k4.z, k[3] = k4.w;
+        if (a.values != nullptr) {
+#if BHT_SPLIT_TMA
+          const uint4 v4 = *reinterpret_cast<const uint4*>(s.in + kSplitTile + at);
+#else
+          const uint4 v4 = __ldcs(reinterpret_cast<const uint4*>(a.values + i0 + at));
+#endif
+          v[0] = v4.x, v[1] = v4.y, v[2] = v4.z, v[3] = v4.w;
+        }
+      } else {
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        dst[j][e] = static_cast<uint32_t>((static_cast<uint64_t>(bucket_index(h0, k[j][e]) >> region_log2) * inv_per) >> 32);
-        rank[j][e] = 0;
-        if (i + e < n) rank[j][e] = atomicAdd(&hist[dst[j][e]], 1u);
-      }
-    }
-    __syncthreads();
-    {
-      const uint32_t h = hist[threadIdx.x];
-      uint32_t x = h;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(kFullMask, x, o);
-        if (lane >= o) x += y;
-      }
-      if (lane == 31) warp_tot[warp] = x;
-      __syncthreads();
-      uint32_t before = 0;
-      for (int w = 0; w < warp; ++w) before += warp_tot[w];
-      tile_off[threadIdx.x] = before + x - h;
-      base_of[threadIdx.x] = (h != 0 && threadIdx.x < n_groups) ? atomicAdd(&group_cursor[threadIdx.x], h) : 0u;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int j = 0; j < kGroups; ++j) {
-      const uint64_t i = i0 + (static_cast<uint64_t>(j) * kSplitBlock + threadIdx.x) * 4;
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        if (i + e < n) {
-          const uint32_t slot = tile_off[dst[j][e]] + rank[j][e];
-          s_pair[slot] = make_uint2(k[j][e], v[j][e]);
-          s_dest[slot] = static_cast<uint8_t>(dst[j][e]);
+        for (int e = 0; e < 4; ++e) {
+          const bool in = at + e < len;
+          k[e] = in ? __ldcs(a.keys + i0 + at + e) : 0u;
+          v[e] = (in && a.values != nullptr) ? __ldcs(a.values + i0 + at + e) : 0u;
         }
       }
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        if (a.values == nullptr) v[e] = value_for_key(k[e]);  // kernel-uniform
+        kv[4 * j + e] = make_uint2(k[e], v[e]);
+        valid |= (at + e < len) ? 1u << (4 * j + e) : 0u;
+      }
     }
-    __syncthreads();
-    const uint32_t in_tile = static_cast<uint32_t>(n - i0 < kSplitTile ? n - i0 : kSplitTile);
 #pragma unroll
     for (int j = 0; j < kSplitPerThread; ++j) {
-      const uint32_t slot = j * kSplitBlock + threadIdx.x;
-      const bool in = slot < in_tile;
-      uint2 out = make_uint2(0u, 0u);
-      bool fits = false;
-      if (in) {
-        const uint32_t d = s_dest[slot];
-        const uint32_t pos = base_of[d] + (slot - tile_off[d]);
-        out = s_pair[slot];
-        fits = pos < group_cap;
-        if (fits) __stcs(grouped + static_cast<uint64_t>(d) * group_cap + pos, out);
-      }
-      spill_append(in && !fits, out, sp, lane);
+      const uint32_t d = group_of(kv[j].x);
+      uint32_t rank = 0;
+      if ((valid >> j) & 1u) rank = atomicAdd(&s.hist[d], 1u);
+      dr[j] = d | (rank << 8);
     }
-    __syncthreads();
+    __syncthreads();  // every rank of the tile is taken, and `in` has been read by everyone
+    fetch(tile + gridDim.x);
+    if (full) split_tile_finish<true>(s, kv, dr, valid, len, a.n_groups, 0u, a.group_cap, a.group_cursor, a.grouped, a.sp, tile, group_of);
+    else split_tile_finish<false>(s, kv, dr, valid, len, a.n_groups, 0u, a.group_cap, a.group_cursor, a.grouped, a.sp, tile, group_of);
   }
 }
 
 // ---- K10 ------------------------------------------------------------------------------------------------------
-// grouped: segment g = pairs of group g (fine regions [g * per, (g + 1) * per)), group_cursor[g] of them (clamped to
-// group_cap).  bins[f * cap ..] / bin_cursor[f]: the bin of fine region f.  A tile never leaves its group.
-__global__ void __launch_bounds__(kSplitBlock)
-bin_split_kernel(const __grid_constant__ HashFn h0, uint32_t region_log2, uint32_t per, uint32_t n_groups, uint32_t n_regions,
-                 uint32_t cap, uint32_t group_cap, const uint2* __restrict__ grouped, const uint32_t* __restrict__ group_cursor,
-                 uint32_t* __restrict__ bin_cursor, uint2* __restrict__ bins, const Spill sp) {
-  __shared__ uint2 s_pair[kSplitTile];
-  __shared__ uint8_t s_local[kSplitTile];
-  __shared__ uint32_t hist[256], tile_off[256], base_of[256], warp_tot[kSplitBlock / 32];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint32_t tiles_per_group = (group_cap + kSplitTile - 1) / kSplitTile;
-  const uint64_t n_tiles = static_cast<uint64_t>(n_groups) * tiles_per_group;
-  for (uint64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-    const uint32_t g = static_cast<uint32_t>(tile / tiles_per_group);
-    const uint32_t t0 = static_cast<uint32_t>(tile % tiles_per_group) * kSplitTile;
-    const uint32_t in_group = min(group_cursor[g], group_cap);
-    if (t0 >= in_group) continue;  // block-uniform
-    const uint32_t len = min(static_cast<uint32_t>(kSplitTile), in_group - t0);
-    const uint2* src = grouped + static_cast<uint64_t>(g) * group_cap + t0;
-    const uint32_t f_base = g * per;
-    hist[threadIdx.x] = 0;
-    __syncthreads();
+// Second partition level.  grouped: segment g = pairs of group g (fine regions [g * per, (g + 1) * per)),
+// group_cursor[g] of them (clamped to group_cap).  bins[f * cap ..] / bin_cursor[f]: the bin of fine region f.  A tile
+// never leaves its group, so it has at most `per` <= 256 destinations and its runs are ~25 pairs = 200 contiguous bytes.
+struct BinArgs {
+  HashFn h0;
+  uint32_t region_log2, per, n_groups, n_regions, cap, group_cap;
+  const uint2* grouped;
+  const uint32_t* group_cursor;
+  uint32_t* bin_cursor;
+  uint2* bins;
+  Spill sp;
+};
 
+__global__ void __launch_bounds__(kSplitBlock, BHT_SPLIT_CTAS)
+bin_split_kernel(const __grid_constant__ BinArgs a) {
+  extern __shared__ __align__(16) unsigned char split_bytes[];
+  SplitShared& s = *reinterpret_cast<SplitShared*>(split_bytes);
+  if (threadIdx.x < 256) s.hist[threadIdx.x] = 0;
+  if (threadIdx.x == 0) mbar_init(&s.mbar);
+  __syncthreads();
+  const uint32_t tiles_per_group = (a.group_cap + kSplitTile - 1) / kSplitTile;
+  const uint64_t n_tiles = static_cast<uint64_t>(a.n_groups) * tiles_per_group;
+  // the tiles of this CTA: every gridDim.x-th one that holds pairs (the segments are sized for mean + 6 sigma)
+  struct Tile {
+    uint64_t id;
+    uint32_t g, t0, len;
+  };
+  auto next_tile = [&](uint64_t from) {
+    Tile t{from, 0u, 0u, 0u};
+    for (; t.id < n_tiles; t.id += gridDim.x) {
+      t.g = static_cast<uint32_t>(t.id / tiles_per_group);
+      t.t0 = static_cast<uint32_t>(t.id % tiles_per_group) * kSplitTile;
+      const uint32_t in_group = min(a.group_cursor[t.g], a.group_cap);
+      if (t.t0 < in_group) {
+        t.len = min(static_cast<uint32_t>(kSplitTile), in_group - t.t0);
+        break;
+      }
+    }
+    return t;
+  };
+  auto fetch = [&](const Tile& t) {
+#if BHT_SPLIT_TMA
+    if (threadIdx.x == 0 && t.id < n_tiles && t.len == kSplitTile) {
+      mbar_expect(&s.mbar, kSplitTile * 8u);
+      bulk_load(s.in, a.grouped + static_cast<uint64_t>(t.g) * a.group_cap + t.t0, kSplitTile * 8u, &s.mbar);  // 16-byte aligned: group_cap is even
+    }
+#endif
+  };
+  uint32_t parity = 0;
+  Tile cur = next_tile(blockIdx.x);
+  fetch(cur);
+  while (cur.id < n_tiles) {
+    const Tile nxt = next_tile(cur.id + gridDim.x);
+    const bool full = cur.len == kSplitTile;
+    const uint2* src = a.grouped + static_cast<uint64_t>(cur.g) * a.group_cap + cur.t0;  // 16-byte aligned: group_cap is even
+    const uint32_t f_base = cur.g * a.per;
+    const uint32_t n_dest = min(a.per, a.n_regions - f_base);
+    auto region_of = [&](uint32_t key) { return ((bucket_index(a.h0, key) >> a.region_log2) - f_base) & 255u; };  // < per <= 256
     uint2 kv[kSplitPerThread];
-    uint32_t local[kSplitPerThread], rank[kSplitPerThread];
-#pragma unroll
-    for (int j = 0; j < kSplitPerThread; ++j) {
-      const uint32_t i = j * kSplitBlock + threadIdx.x;
-      kv[j] = i < len ? __ldcs(src + i) : make_uint2(0u, 0u);
+    uint32_t dr[kSplitPerThread];
+    uint32_t valid = 0;
+#if BHT_SPLIT_TMA
+    if (full) {
+      mbar_wait(&s.mbar, parity);
+      parity ^= 1u;
     }
+#endif
 #pragma unroll
-    for (int j = 0; j < kSplitPerThread; ++j) {
-      const uint32_t i = j * kSplitBlock + threadIdx.x;
-      local[j] = (bucket_index(h0, kv[j].x) >> region_log2) - f_base;  // < per <= 256 for every pair of the group
-      rank[j] = 0;
-      if (i < len && local[j] < 256u) rank[j] = atomicAdd(&hist[local[j]], 1u);
-    }
-    __syncthreads();
-    // exclusive scan of hist + one global reservation per destination of the tile
-    {
-      const uint32_t h = hist[threadIdx.x];
-      uint32_t x = h;
+    for (int j = 0; j < kSplitPerThread / 2; ++j) {
+      const uint32_t at = (j * kSplitBlock + threadIdx.x) * 2;  // this thread's two consecutive pairs
+      if (full) {
+#if BHT_SPLIT_TMA
+        const uint4 two = *reinterpret_cast<const uint4*>(s.in + 2 * at);
+#else
+        const uint4 two = __ldcs(reinterpret_cast<const uint4*>(src + at));
+#endif
+        kv[2 * j] = make_uint2(two.x, two.y);
+        kv[2 * j + 1] = make_uint2(two.z, two.w);
+      } else {
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(kFullMask, x, o);
-        if (lane >= o) x += y;
+        for (int e = 0; e < 2; ++e) kv[2 * j + e] = at + e < cur.len ? __ldcs(src + at + e) : make_uint2(0u, 0u);
       }
-      if (lane == 31) warp_tot[warp] = x;
-      __syncthreads();
-      uint32_t before = 0;
-      for (int w = 0; w < warp; ++w) before += warp_tot[w];
-      tile_off[threadIdx.x] = before + x - h;
-      const uint32_t f = f_base + threadIdx.x;
-      base_of[threadIdx.x] = (h != 0 && f < n_regions) ? atomicAdd(&bin_cursor[f], h) : 0u;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) valid |= (at + e < cur.len) ? 1u << (2 * j + e) : 0u;
     }
-    __syncthreads();
 #pragma unroll
     for (int j = 0; j < kSplitPerThread; ++j) {
-      const uint32_t i = j * kSplitBlock + threadIdx.x;
-      if (i < len && local[j] < 256u) {
-        const uint32_t slot = tile_off[local[j]] + rank[j];
-        s_pair[slot] = kv[j];
-        s_local[slot] = static_cast<uint8_t>(local[j]);
-      }
+      const uint32_t d = region_of(kv[j].x);
+      uint32_t rank = 0;
+      if ((valid >> j) & 1u) rank = atomicAdd(&s.hist[d], 1u);
+      dr[j] = d | (rank << 8);
     }
-    __syncthreads();
-#pragma unroll
-    for (int j = 0; j < kSplitPerThread; ++j) {
-      const uint32_t slot = j * kSplitBlock + threadIdx.x;
-      const bool in = slot < len;
-      uint2 out = make_uint2(0u, 0u);
-      bool fits = false;
-      if (in) {
-        const uint32_t l = s_local[slot];
-        const uint32_t pos = base_of[l] + (slot - tile_off[l]);
-        out = s_pair[slot];
-        fits = pos < cap;
-        if (fits) bins[static_cast<uint64_t>(f_base + l) * cap + pos] = out;
-      }
-      spill_append(in && !fits, out, sp, lane);
-    }
-    __syncthreads();
+    __syncthreads();  // every rank of the tile is taken, and `in` has been read by everyone
+    fetch(nxt);
+    if (full) split_tile_finish<true>(s, kv, dr, valid, cur.len, n_dest, f_base, a.cap, a.bin_cursor, a.bins, a.sp, cur.id, region_of);
+    else split_tile_finish<false>(s, kv, dr, valid, cur.len, n_dest, f_base, a.cap, a.bin_cursor, a.bins, a.sp, cur.id, region_of);
+    cur = nxt;
   }
 }
 
 // ---- K11 ------------------------------------------------------------------------------------------------------
+// One 16-byte unit of a bin = two pairs.  GUARD: the unit may lie (partly) past the end of the bin.
+template <bool GUARD>
+__device__ __forceinline__ uint32_t claim_unit(const uint4 v, uint32_t q, uint32_t n_r, const HashFn& h0, uint32_t first32,
+                                               uint32_t nb, uint32_t b_log2, uint32_t B, unsigned long long* rows, uint32_t* cnt) {
+  uint32_t spilled = 0;
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {
+    const uint32_t k = e ? v.z : v.x, val = e ? v.w : v.y;
+    if (!GUARD || 2u * q + e < n_r) {
+      const uint32_t lb = bucket_index(h0, k) - first32;  // < nb: the bin holds pairs of this region only
+#if defined(BHT_EXP_NOSTORE) || defined(BHT_EXP_LINEAR)
+      if (lb >= nb) continue;  // the experiments feed this kernel garbage
+#endif
+      const uint32_t slot = atomicAdd(&cnt[lb], 1u);
+      if (slot < B) rows[(lb << b_log2) + slot] = pack_pair(k, val);
+      else spilled |= 1u << e;
+    }
+  }
+  return spilled;
+}
+
 __global__ void __launch_bounds__(kBuildBlock)
 region_build_kernel(const __grid_constant__ TableView t, uint32_t region_log2, uint32_t b_log2, uint32_t cap,
                     const uint32_t* __restrict__ bin_cursor, const uint2* __restrict__ bins, int fresh, const Spill sp,
-                    DevCounters* __restrict__ ctr) {
+                    DevCounters* __restrict__ ctr, uint32_t ahead) {
   extern __shared__ __align__(16) unsigned char sm_bytes[];
   const uint32_t region_buckets = 1u << region_log2;
   const uint32_t B = 1u << b_log2;
   unsigned long long* rows = reinterpret_cast<unsigned long long*>(sm_bytes);  // region_buckets * B slots
   uint32_t* cnt = reinterpret_cast<uint32_t*>(sm_bytes + (static_cast<size_t>(region_buckets) << (b_log2 + 3)));
-  uint2* stash = reinterpret_cast<uint2*>(cnt + region_buckets);
-  __shared__ uint32_t stash_count, placed_count, hole_count;
+  uint16_t* stash = reinterpret_cast<uint16_t*>(cnt + region_buckets);  // positions (in the bin) of the pairs whose bucket was full
+  __shared__ uint32_t stash_count, hole_count;
   __shared__ unsigned long long stash_base;
-  const int lane = threadIdx.x & 31;
   const uint32_t region = blockIdx.x;
   const uint64_t first = static_cast<uint64_t>(region) << region_log2;
+  const uint32_t first32 = static_cast<uint32_t>(first);
   const uint32_t nb = static_cast<uint32_t>(min(static_cast<uint64_t>(region_buckets), t.num_buckets - first));
   const uint32_t n_slots = nb << b_log2;
   unsigned long long* gstore = reinterpret_cast<unsigned long long*>(t.store) + (first << b_log2);  // 64 KiB-aligned offset
+
+  // The bin of the region `ahead` CTAs later (the CTA that takes this one's place on the SM, roughly) goes to the L2
+  // now, so that phase 1 of that CTA reads L2 hits.
+  if (ahead != 0 && region + ahead < gridDim.x) {
+    const uint32_t r2 = region + ahead;
+    const uint32_t bytes = min(bin_cursor[r2], cap) * 8u;
+    const char* base = reinterpret_cast<const char*>(bins + static_cast<uint64_t>(r2) * cap);
+    for (uint32_t off = threadIdx.x * 128u; off < bytes; off += kBuildBlock * 128u) prefetch_l2(base + off);
+  }
 
   // phase 0: the region's buckets into shared memory
   {
@@ -316,7 +468,7 @@ region_build_kernel(const __grid_constant__ TableView t, uint32_t region_log2, u
       if ((n_slots & 1u) && threadIdx.x == 0) rows[n_slots - 1] = gstore[n_slots - 1];
     }
     for (uint32_t i = threadIdx.x; i < nb; i += kBuildBlock) cnt[i] = 0;
-    if (threadIdx.x == 0) stash_count = placed_count = hole_count = 0;
+    if (threadIdx.x == 0) stash_count = hole_count = 0;
   }
   __syncthreads();
   if (!fresh) {
@@ -329,68 +481,59 @@ region_build_kernel(const __grid_constant__ TableView t, uint32_t region_log2, u
     __syncthreads();
   }
 
-  // phase 1: every pair of the bin claims slot = load++ of its bucket
+  // phase 1: every pair of the bin claims slot = load++ of its bucket (a shared-memory atomic: no CAS, no lost race).
+  // Two pairs per 16-byte load, BHT_BUILD_U pairs in flight per thread.  A pair whose bucket is full only leaves a bit
+  // in `spilled`; after the unrolled block the thread notes the bin positions of those pairs in the CTA's stash.
   const uint32_t n_r = min(bin_cursor[region], cap);
-  const uint2* bin = bins + static_cast<uint64_t>(region) * cap;
-  uint32_t n_ins = 0;
-  constexpr int U = BHT_BUILD_U;  // pairs in flight per thread: a 64 KiB region holds ~29 pairs per thread at load factor 0.9
-  for (uint32_t i0 = threadIdx.x; i0 - lane < n_r; i0 += kBuildBlock * U) {  // warp-uniform trip count
-    uint2 kv[U];
-    bool in[U];
+  const uint2* bin = bins + static_cast<uint64_t>(region) * cap;  // 16-byte aligned: cap is even
+  const uint4* bin4 = reinterpret_cast<const uint4*>(bin);
+  const uint32_t n_units = (n_r + 1u) >> 1;
+  constexpr int U = BHT_BUILD_U / 2;
+  for (uint32_t q0 = threadIdx.x; q0 < n_units; q0 += kBuildBlock * U) {
+    uint32_t spilled = 0;
+    if (2u * (q0 + (U - 1) * kBuildBlock) + 1u < n_r) {  // every pair of the thread's U units exists: no predicates
+      uint4 v[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const uint32_t i = i0 + u * kBuildBlock;
-      in[u] = i < n_r;
-      kv[u] = make_uint2(0u, 0u);
-      if (in[u]) kv[u] = __ldcs(bin + i);
-    }
+      for (int u = 0; u < U; ++u) v[u] = __ldcs(bin4 + q0 + u * kBuildBlock);
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      bool spilled = false;
-      if (in[u]) {
-        const uint32_t lb = bucket_index(t.h[0], kv[u].x) - static_cast<uint32_t>(first);
-        const uint32_t slot = lb < nb ? atomicAdd(&cnt[lb], 1u) : B;
-        if (slot < B) {
-          rows[(lb << b_log2) + slot] = pack_pair(kv[u].x, kv[u].y);
-          ++n_ins;
-        } else {
-          spilled = true;
-        }
+      for (int u = 0; u < U; ++u)
+        spilled |= claim_unit<false>(v[u], q0 + u * kBuildBlock, n_r, t.h[0], first32, nb, b_log2, B, rows, cnt) << (2 * u);
+    } else {
+      uint4 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t q = q0 + u * kBuildBlock;
+        v[u] = make_uint4(0u, 0u, 0u, 0u);
+        if (q < n_units) v[u] = __ldcs(bin4 + q);  // an odd bin's last unit reads one pair of slack inside the bin's capacity
       }
-      // spilled pairs: into the CTA's stash (one shared-memory atomic per warp); past its end, straight to the list
-      const uint32_t m = __ballot_sync(kFullMask, spilled);
-      if (m != 0) {
-        const int leader = __ffs(m) - 1;
-        uint32_t base = 0;
-        if (lane == leader) base = atomicAdd(&stash_count, static_cast<uint32_t>(__popc(m)));
-        base = __shfl_sync(kFullMask, base, leader);
-        const uint32_t pos = base + __popc(m & ((1u << lane) - 1u));
-        const bool stashed = spilled && pos < kStashPairs;
-        if (stashed) stash[pos] = kv[u];
-        spill_append(spilled && !stashed, kv[u], sp, lane);
-      }
-    }
-  }
-  {  // one set of global counter updates per CTA (not per warp: thousands of CTAs would hammer three addresses)
-    uint32_t w = n_ins;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(kFullMask, w, o);
-    if (lane == 0 && w != 0) atomicAdd(&placed_count, w);
+      for (int u = 0; u < U; ++u)
+        spilled |= claim_unit<true>(v[u], q0 + u * kBuildBlock, n_r, t.h[0], first32, nb, b_log2, B, rows, cnt) << (2 * u);
+    }
+    while (spilled != 0) {
+      const uint32_t bit = __ffs(spilled) - 1u;
+      spilled &= spilled - 1u;
+      const uint32_t idx = 2u * (q0 + (bit >> 1) * kBuildBlock) + (bit & 1u);
+      const uint32_t pos = atomicAdd(&stash_count, 1u);
+      if (pos < kStashPairs) stash[pos] = static_cast<uint16_t>(idx);
+      else spill_fresh(bin[idx], sp);  // past the stash: straight to the list, untouched
+    }
   }
   __syncthreads();  // every claimed slot is written
 
   // phase 1b: the first eviction of the stashed pairs, in shared memory (table.cpp:67-81): the pair goes into a random
   // slot of its full bucket, the victim goes to the spill list with the bucket named by the hash function after the
   // lowest-index one that maps it here, and a chain length of 1.  One probe (the inspection that found the bucket full).
-  const uint32_t stashed = min(stash_count, kStashPairs);
+  const uint32_t spilled_total = stash_count;
+  const uint32_t stashed = min(spilled_total, kStashPairs);
   if (threadIdx.x == 0 && stashed != 0) stash_base = atomicAdd(sp.cursor, static_cast<unsigned long long>(stashed));
   __syncthreads();
   if (stashed != 0) {
     uint64_t rng = xorshift_init(mix_seed(t.seed, 0x626C6B64ull + static_cast<uint64_t>(blockIdx.x) * kBuildBlock + threadIdx.x));
     for (uint32_t i = threadIdx.x; i < stashed; i += kBuildBlock) {
-      const uint2 p = stash[i];
+      const uint2 p = bin[stash[i]];
       const uint32_t bid = bucket_index(t.h[0], p.x);
-      const uint32_t lb = bid - static_cast<uint32_t>(first);
+      const uint32_t lb = bid - first32;
       const unsigned long long old = atomicExch(rows + (lb << b_log2) + xorshift_next_below(rng, B), pack_pair(p.x, p.y));
       const uint32_t vk = static_cast<uint32_t>(old);
       uint32_t next = 0;
@@ -435,13 +578,15 @@ region_build_kernel(const __grid_constant__ TableView t, uint32_t region_log2, u
     for (uint32_t i = threadIdx.x; i < n4; i += kBuildBlock) g4[i] = rows4[i];
 #endif
     if ((n_slots & 1u) && threadIdx.x == 0) gstore[n_slots - 1] = rows[n_slots - 1];
-    if (threadIdx.x == 0 && (placed_count != 0 || stashed != 0)) {
-      const unsigned long long a = static_cast<unsigned long long>(placed_count) + hole_count;
+    if (threadIdx.x == 0 && n_r != 0) {
+      // one set of global counter updates per CTA.  Every pair of the bin was either placed or noted in `stash_count`.
+      const unsigned long long placed = n_r - spilled_total;
+      const unsigned long long a = placed + hole_count;
       if (a != 0) {
         atomicAdd(&ctr->inserted, a);
         atomicAdd(&ctr->inserted_total, a);
       }
-      atomicAdd(&ctr->insert_probes, static_cast<unsigned long long>(placed_count) + stashed);
+      atomicAdd(&ctr->insert_probes, placed + stashed);
     }
 #if BHT_BUILD_TMA_STORE
     asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // shared memory may go once the copies have read it
@@ -451,18 +596,20 @@ region_build_kernel(const __grid_constant__ TableView t, uint32_t region_log2, u
 
 }  // namespace
 
-// Geometry of a blocked build of n pairs into table t; n_regions == 0: not applicable.
+// Geometry of a blocked build of up to n pairs into table t; n_regions == 0: not applicable.
 BlockedPlan plan_blocked_build(const TableView& t, uint64_t n) {
   BlockedPlan p{};
   uint32_t b_log2 = 0;
   while ((1u << b_log2) < t.bucket_size) ++b_log2;
   if (b_log2 > 6 || n == 0 || n > 0xFFFFFFFFull) return p;
+  // The first eviction of a pair whose bucket is full happens inside K11; with max_chain == 0 the reference fails that
+  // insertion before any exchange (table.cpp:67), which is the general kernel's business.
+  if (t.max_chain == 0) return p;
   // 64 KiB of slots per fine region (three CTAs of K11 per SM); 128 KiB (one CTA per SM, ~20 % slower) for tables
   // between 4 and 8 GB, so that two partition levels of <= 256 x 256 still reach every region
   uint32_t region_bytes_log2 = kRegionBytesLog2;
   if ((t.num_buckets << (b_log2 + 3)) > (256ull * kMaxShards << kRegionBytesLog2)) region_bytes_log2 = kRegionBytesLog2 + 1;
-  if (const char* e = std::getenv("BHT_REGION_BYTES_LOG2")) region_bytes_log2 = static_cast<uint32_t>(std::atoi(e));  // tuning knob
-  if (region_bytes_log2 < 12 || region_bytes_log2 > 17 || region_bytes_log2 < 3 + b_log2 + 5) return p;
+  if (region_bytes_log2 < 3 + b_log2 + 5) return p;
   const uint32_t region_log2 = region_bytes_log2 - 3 - b_log2;
   const uint64_t regions = (t.num_buckets + (1ull << region_log2) - 1) >> region_log2;
   if (regions > 256ull * kMaxShards || t.num_buckets > 0x7FFFFFFFull) return p;  // two levels of <= 256 x 256; 31-bit start buckets
@@ -474,6 +621,7 @@ BlockedPlan plan_blocked_build(const TableView& t, uint64_t n) {
   const double mean = static_cast<double>(n) * static_cast<double>(1ull << region_log2) / static_cast<double>(t.num_buckets);
   double cap = mean + 6.0 * std::sqrt(mean) + 32.0;
   if (cap > static_cast<double>(n)) cap = static_cast<double>(n);
+  if (cap > 65000.0) return p;  // K11 notes bin positions in 16 bits (a bin holds about what its 64 / 128 KiB region holds)
   p.cap = (static_cast<uint32_t>(cap) + 2u) & ~1u;  // even: every bin starts 16-byte aligned
   p.n_regions = static_cast<uint32_t>(regions);
   p.region_log2 = region_log2;
@@ -484,6 +632,9 @@ BlockedPlan plan_blocked_build(const TableView& t, uint64_t n) {
   double gcap = gmean + 6.0 * std::sqrt(gmean) + 64.0;
   if (gcap > static_cast<double>(n)) gcap = static_cast<double>(n);
   p.group_cap = (static_cast<uint32_t>(gcap) + 2u) & ~1u;
+  // the partition passes address their outputs with 32-bit indices
+  if (static_cast<uint64_t>(p.n_groups) * p.group_cap >= 0xFFFFFFFFull || static_cast<uint64_t>(p.n_regions) * p.cap >= 0xFFFFFFFFull)
+    return BlockedPlan{};
   return p;
 }
 
@@ -494,51 +645,92 @@ size_t blocked_scratch_bytes(const BlockedPlan& p, uint64_t n) {
          (static_cast<size_t>(p.n_regions) + p.n_groups) * 4 + 16 + n * 4 + 64;
 }
 
+namespace {
+struct ScratchMap {
+  uint2 *grouped, *bins, *spill;
+  unsigned long long* spill_cursor;
+  uint32_t *bin_cursor, *group_cursor, *spill_start;
+};
+ScratchMap map_scratch(const BlockedPlan& p, uint64_t n, void* scratch) {
+  ScratchMap m;
+  m.grouped = reinterpret_cast<uint2*>(scratch);
+  m.bins = m.grouped + static_cast<size_t>(p.n_groups) * p.group_cap;
+  m.spill = m.bins + static_cast<size_t>(p.n_regions) * p.cap;
+  m.spill_cursor = reinterpret_cast<unsigned long long*>(m.spill + n);
+  m.bin_cursor = reinterpret_cast<uint32_t*>(m.spill_cursor + 2);
+  m.group_cursor = m.bin_cursor + p.n_regions;
+  m.spill_start = reinterpret_cast<uint32_t*>(
+      (reinterpret_cast<uintptr_t>(m.group_cursor + p.n_groups) + 15) & ~static_cast<uintptr_t>(15));
+  return m;
+}
+}  // namespace
+
+// A blocked build in three steps, so that a batch may arrive in chunks (host buffers over PCIe, the receive side of a
+// sharded build): begin zeroes the cursors, scatter runs K8g over one chunk (any number of times, at most n pairs in
+// total), finish runs K10 + K11 and hands the spill list to the caller.
+cudaError_t blocked_build_begin(const BlockedPlan& p, uint64_t n, void* scratch, cudaStream_t stream) {
+  const ScratchMap m = map_scratch(p, n, scratch);
+  return cudaMemsetAsync(m.spill_cursor, 0, 16 + (static_cast<size_t>(p.n_regions) + p.n_groups) * 4, stream);
+}
+
+cudaError_t blocked_build_scatter(const TableView& t, const BlockedPlan& p, uint64_t n, void* scratch, const uint32_t* keys,
+                                  const uint32_t* values, uint64_t len, int sm_count, cudaStream_t stream) {
+  if (len == 0) return cudaSuccess;
+  const ScratchMap m = map_scratch(p, n, scratch);
+  const Spill sp{m.spill, m.spill_start, m.spill_cursor};
+  const bool aligned = ((reinterpret_cast<uintptr_t>(keys) | reinterpret_cast<uintptr_t>(values)) & 15) == 0;  // values may be null
+  const uint32_t inv_per = static_cast<uint32_t>((1ull << 32) / p.per) + 1u;  // exact quotient for fine ids < 2^16, per <= 256
+  const uint64_t tiles = (len + kSplitTile - 1) / kSplitTile;
+  const int grid = static_cast<int>(std::min<uint64_t>(tiles, static_cast<uint64_t>(sm_count) * BHT_SPLIT_CTAS));
+  static const cudaError_t attr = cudaFuncSetAttribute(group_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                      static_cast<int>(sizeof(SplitShared)));
+  if (attr != cudaSuccess) return attr;
+  const GroupArgs ga{t.h[0], p.region_log2, inv_per, p.n_groups, p.group_cap, keys, values, len, m.group_cursor, m.grouped, sp, aligned ? 1 : 0};
+  group_scatter_kernel<<<grid, kSplitBlock, sizeof(SplitShared), stream>>>(ga);
+  note_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t blocked_build_finish(const TableView& t, const BlockedPlan& p, uint64_t n, void* scratch, bool fresh,
+                                 DevCounters* ctr, int sm_count, cudaStream_t stream, PairSource* spill_out,
+                                 const unsigned long long** spill_count_out) {
+  const ScratchMap m = map_scratch(p, n, scratch);
+  const Spill sp{m.spill, m.spill_start, m.spill_cursor};
+  const uint64_t tiles_b = static_cast<uint64_t>(p.n_groups) * ((p.group_cap + kSplitTile - 1) / kSplitTile);
+  const int grid_b = static_cast<int>(std::min<uint64_t>(tiles_b, static_cast<uint64_t>(sm_count) * BHT_SPLIT_CTAS));
+  static const cudaError_t attr = cudaFuncSetAttribute(bin_split_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                      static_cast<int>(sizeof(SplitShared)));
+  if (attr != cudaSuccess) return attr;
+  const BinArgs ba{t.h[0], p.region_log2, p.per, p.n_groups, p.n_regions, p.cap, p.group_cap, m.grouped, m.group_cursor, m.bin_cursor, m.bins, sp};
+  bin_split_kernel<<<grid_b, kSplitBlock, sizeof(SplitShared), stream>>>(ba);
+  note_launch();
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+
+  const int smem_c = static_cast<int>((8u << (p.region_log2 + p.b_log2)) + (4u << p.region_log2) + kStashPairs * 2);
+  e = cudaFuncSetAttribute(region_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_c);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+#ifdef BHT_BUILD_PREFETCH  // measured (profiles/r02d_*): +200 MB of DRAM reads (the prefetched lines are fetched twice), no gain
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, region_build_kernel, kBuildBlock, smem_c) != cudaSuccess) per_sm = 1;
+#endif
+  region_build_kernel<<<p.n_regions, kBuildBlock, smem_c, stream>>>(t, p.region_log2, p.b_log2, p.cap, m.bin_cursor, m.bins,
+                                                                   fresh ? 1 : 0, sp, ctr, static_cast<uint32_t>(per_sm * sm_count));
+  note_launch();
+  spill_out->keys = reinterpret_cast<const uint32_t*>(m.spill);
+  spill_out->values = nullptr;
+  spill_out->start = m.spill_start;
+  *spill_count_out = m.spill_cursor;
+  return cudaGetLastError();
+}
+
 cudaError_t launch_blocked_build(const TableView& t, const BlockedPlan& p, const uint32_t* keys, const uint32_t* values,
                                  uint64_t n, bool fresh, void* scratch, DevCounters* ctr, int sm_count, cudaStream_t stream,
                                  PairSource* spill_out, const unsigned long long** spill_count_out) {
-  unsigned char* s = static_cast<unsigned char*>(scratch);
-  uint2* grouped = reinterpret_cast<uint2*>(s);
-  uint2* bins = grouped + static_cast<size_t>(p.n_groups) * p.group_cap;
-  uint2* spill = bins + static_cast<size_t>(p.n_regions) * p.cap;
-  unsigned long long* spill_cursor = reinterpret_cast<unsigned long long*>(spill + n);
-  uint32_t* bin_cursor = reinterpret_cast<uint32_t*>(spill_cursor + 2);
-  uint32_t* group_cursor = bin_cursor + p.n_regions;
-  uint32_t* spill_start = reinterpret_cast<uint32_t*>(
-      (reinterpret_cast<uintptr_t>(group_cursor + p.n_groups) + 15) & ~static_cast<uintptr_t>(15));
-  const Spill sp{spill, spill_start, spill_cursor};
-  cudaError_t e = cudaMemsetAsync(spill_cursor, 0, 16 + (static_cast<size_t>(p.n_regions) + p.n_groups) * 4, stream);
-  if (e != cudaSuccess) return e;
-
-  const bool aligned = ((reinterpret_cast<uintptr_t>(keys) | reinterpret_cast<uintptr_t>(values)) & 15) == 0;  // values may be null
-  const uint32_t inv_per = static_cast<uint32_t>((1ull << 32) / p.per) + 1u;  // exact quotient for fine ids < 2^16, per <= 256
-  const uint64_t tiles_a = (n + kSplitTile - 1) / kSplitTile;
-  const int grid_a = static_cast<int>(std::min<uint64_t>(tiles_a, static_cast<uint64_t>(sm_count) * 8));
-  group_scatter_kernel<<<grid_a, kSplitBlock, 0, stream>>>(t.h[0], p.region_log2, inv_per, p.n_groups, p.group_cap, keys, values, n,
-                                                          aligned, group_cursor, grouped, sp);
-  note_launch();
-  e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
-
-  const uint64_t tiles_b = static_cast<uint64_t>(p.n_groups) * ((p.group_cap + kSplitTile - 1) / kSplitTile);
-  const int grid_b = static_cast<int>(std::min<uint64_t>(tiles_b, static_cast<uint64_t>(sm_count) * 8));
-  bin_split_kernel<<<grid_b, kSplitBlock, 0, stream>>>(t.h[0], p.region_log2, p.per, p.n_groups, p.n_regions, p.cap, p.group_cap,
-                                                      grouped, group_cursor, bin_cursor, bins, sp);
-  note_launch();
-  e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
-
-  const int smem_c = static_cast<int>((8u << (p.region_log2 + p.b_log2)) + (4u << p.region_log2) + kStashPairs * 8);
-  e = cudaFuncSetAttribute(region_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_c);
-  if (e != cudaSuccess) return e;
-  region_build_kernel<<<p.n_regions, kBuildBlock, smem_c, stream>>>(t, p.region_log2, p.b_log2, p.cap, bin_cursor, bins,
-                                                                   fresh ? 1 : 0, sp, ctr);
-  note_launch();
-  spill_out->keys = reinterpret_cast<const uint32_t*>(spill);
-  spill_out->values = nullptr;
-  spill_out->start = spill_start;
-  *spill_count_out = spill_cursor;
-  return cudaGetLastError();
+  cudaError_t e = blocked_build_begin(p, n, scratch, stream);
+  if (e == cudaSuccess) e = blocked_build_scatter(t, p, n, scratch, keys, values, n, sm_count, stream);
+  if (e == cudaSuccess) e = blocked_build_finish(t, p, n, scratch, fresh, ctr, sm_count, stream, spill_out, spill_count_out);
+  return e;
 }
 
 }  // namespace bht_b200

@@ -5,9 +5,12 @@
 //
 //   mod p   p = 2^32 - 5, so 2^32 = 5 (mod p).  x = a*k + b < 2^64 is folded twice,
 //           x -> 5*hi(x) + lo(x) < 6*2^32 -> 5*hi + lo < 2^32 + 25, followed by ONE conditional
-//           subtraction of p (z - p = z + 5 - 2^32, and z < 2p).
-//   mod L   Lemire/Kaser/Kurz "fastmod": with M = ceil(2^64 / L), r mod L = mulhi64(M*r mod 2^64, L)
-//           exactly for every 32-bit r and L.  M is precomputed on the host per hash function.
+//           subtraction of p (z - p = z + 5 - 2^32, and z < 2p).  On the device the three multiply-adds are
+//           written with carry chains (mad.lo.cc / madc.hi), 10 integer instructions.
+//   mod L   q' = mulhi32(r, floor(2^32 / L)) is floor(r / L) or one less (the reciprocal is short by less than
+//           2^-32 per unit of r, and r < 2^32), so r - q'*L is in [0, 2L) and one unsigned min with itself
+//           minus L finishes: 4 instructions (IMAD.HI, IMAD, VIADDMNMX), against 6 64-bit ones for Lemire's
+//           exact 64-bit reciprocal.  The reciprocal is precomputed on the host per hash function.
 //
 // The same code compiles for the host (bht_bucket_index_host) so the CPU tests can check the
 // arithmetic against the oracle without a GPU.
@@ -24,8 +27,8 @@ struct HashFn {
   uint32_t alpha;  // < 2^32 (the reference draws alpha in [1, p-1], keygen.cpp:20)
   uint32_t beta;   // < 2^32 (beta in [0, p-1], keygen.cpp:21)
   uint32_t range;  // L, 1 <= L < 2^32
-  uint32_t pad;
-  uint64_t magic;  // ceil(2^64 / L) mod 2^64  (0 when L == 1)
+  uint32_t recip;  // floor(2^32 / L), saturated to 2^32 - 1 for L == 1
+  uint64_t pad;
 };
 
 inline HashFn make_hash_fn(uint64_t alpha, uint64_t beta, uint64_t range) {
@@ -33,31 +36,44 @@ inline HashFn make_hash_fn(uint64_t alpha, uint64_t beta, uint64_t range) {
   h.alpha = static_cast<uint32_t>(alpha);
   h.beta = static_cast<uint32_t>(beta);
   h.range = static_cast<uint32_t>(range);
+  const uint64_t q = (1ull << 32) / range;
+  h.recip = q > 0xFFFFFFFFull ? 0xFFFFFFFFu : static_cast<uint32_t>(q);  // L == 1: r - (r - 1) = 1, then min(1, 0) = 0
   h.pad = 0;
-  h.magic = 0xFFFFFFFFFFFFFFFFull / range + 1ull;  // wraps to 0 for range == 1, which yields 0
   return h;
 }
 
 // (alpha*key + beta) mod p, result in [0, p).
 __host__ __device__ __forceinline__ uint32_t linear_mod_prime(uint32_t alpha, uint32_t beta, uint32_t key) {
-  const uint64_t x = static_cast<uint64_t>(alpha) * key + beta;                    // IMAD.WIDE
+#ifdef __CUDA_ARCH__
+  uint32_t lo, hi, ylo, yhi, zlo, carry;
+  asm("mad.lo.cc.u32 %0, %2, %3, %4;\n\tmadc.hi.u32 %1, %2, %3, 0;" : "=r"(lo), "=r"(hi) : "r"(alpha), "r"(key), "r"(beta));  // x
+  asm("mad.lo.cc.u32 %0, %2, 5, %3;\n\tmadc.hi.u32 %1, %2, 5, 0;" : "=r"(ylo), "=r"(yhi) : "r"(hi), "r"(lo));  // y = 5*hi(x) + lo(x)
+  asm("mad.lo.cc.u32 %0, %2, 5, %3;\n\taddc.u32 %1, 0, 0;" : "=r"(zlo), "=r"(carry) : "r"(yhi), "r"(ylo));      // z = 5*hi(y) + lo(y)
+  return (carry != 0u || zlo >= static_cast<uint32_t>(kPrime)) ? zlo + 5u : zlo;                                  // z - p (mod 2^32)
+#else
+  const uint64_t x = static_cast<uint64_t>(alpha) * key + beta;
   const uint64_t y = (x >> 32) * 5ull + static_cast<uint32_t>(x);                  // < 6 * 2^32
   const uint64_t z = (y >> 32) * 5ull + static_cast<uint32_t>(y);                  // < 2^32 + 25
   uint32_t r = static_cast<uint32_t>(z);
   if (z >= kPrime) r += 5u;                                                        // z - p (mod 2^32)
   return r;
+#endif
 }
 
-// r mod range via the precomputed 64-bit reciprocal; r, range < 2^32.
-__host__ __device__ __forceinline__ uint32_t mod_range(uint32_t r, uint32_t range, uint64_t magic) {
-  const uint64_t low = magic * r;  // mod 2^64
-  const uint64_t t = static_cast<uint64_t>(static_cast<uint32_t>(low)) * range;
-  const uint64_t u = (low >> 32) * range + (t >> 32);  // no overflow: (2^32-1)^2 + 2^32 - 1 < 2^64
-  return static_cast<uint32_t>(u >> 32);
+// r mod range via the precomputed 32-bit reciprocal; r, range < 2^32.
+__host__ __device__ __forceinline__ uint32_t mod_range(uint32_t r, uint32_t range, uint32_t recip) {
+#ifdef __CUDA_ARCH__
+  const uint32_t q = __umulhi(r, recip);
+#else
+  const uint32_t q = static_cast<uint32_t>((static_cast<uint64_t>(r) * recip) >> 32);
+#endif
+  const uint32_t rem = r - q * range;         // in [0, 2 * range)
+  const uint32_t less = rem - range;          // wraps to a huge value when rem < range
+  return rem < less ? rem : less;
 }
 
 __host__ __device__ __forceinline__ uint32_t bucket_index(const HashFn& h, uint32_t key) {
-  return mod_range(linear_mod_prime(h.alpha, h.beta, key), h.range, h.magic);
+  return mod_range(linear_mod_prime(h.alpha, h.beta, key), h.range, h.recip);
 }
 
 // Shard routing of the multi-GPU table: owner = (g(k) * n_shards) >> 32, g = (a*k+b) mod p.
