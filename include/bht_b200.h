@@ -163,6 +163,18 @@ bht_status bht_build(const bht_config* cfg, int32_t device, const uint32_t* keys
                      uint64_t n, int32_t mem_space, int32_t iht_prose_fallback, bht_table** out,
                      bht_insert_result* result, void* stream);
 
+/* A build whose pairs arrive in chunks (device-resident arrays): the loop of build() (table.cpp:231-238 sequential,
+ * :239-271 parallel) with the key set handed over piece by piece — what the receive side of a sharded build and a
+ * host-buffer bht_insert do internally.  bht_build_begin announces at most n_max pairs; bht_build_feed adds a chunk
+ * (values == NULL: value_for_key, as bht_insert) — BHT_CAPACITY_EXCEEDED past n_max; bht_build_end completes the
+ * build and reports the whole of it (result may be NULL; bht_last_insert_result reads it later).  A table that
+ * qualifies for the shared-memory-blocked build takes every chunk through the first partition pass as it is fed and
+ * runs the rest at the end; every other table inserts chunk by chunk.  Between begin and end the table accepts
+ * no bht_insert / bht_clear; finds see the pairs of the chunks a non-blocked table has inserted so far. */
+bht_status bht_build_begin(bht_table* table, uint64_t n_max, void* stream);
+bht_status bht_build_feed(bht_table* table, const uint32_t* keys, const uint32_t* values, uint64_t n, void* stream);
+bht_status bht_build_end(bht_table* table, bht_insert_result* result, void* stream);
+
 /* The reference's per-variant entry points bcht_insert / bp2ht_insert / iht_insert and bcht_find /
  * bp2ht_find / iht_find (table.hpp:84-101): as bht_insert / bht_find, but BHT_KIND_MISMATCH when the
  * table is not of `kind` (require_kind, table.cpp:15-17; BHT_BCHT also accepts a 1cht table). */
@@ -312,6 +324,9 @@ bht_status bht_host_free(void* ptr);
 
 const char* bht_last_error_string(void);
 const char* bht_version_string(void);
+/* The tuning knobs (BHT_* environment variables; csrc/capi.cu: Knobs) are read once per process; this re-reads them
+ * (tests and experiment scripts that change the environment after the library is loaded). */
+void bht_reload_tuning(void);
 /* Number of kernels this library has launched in this process (bench.py's gpu_launches). */
 uint64_t bht_kernel_launch_count(void);
 size_t bht_sizeof_config(void);

@@ -12,7 +12,7 @@ from .table import (  # noqa: E402
     EMPTY_KEY, EMPTY_SLOT, EMPTY_VALUE, KINDS, OP_FIND, OP_INSERT, BuildOutcome, CapacityError, CudaError, FindStats,
     HashTable, KindMismatchError, bucket_index, build, craft_config, default_max_chain, generate_unique_keys,
     hash_count, hash_keys, hash_table, kernel_launch_count, make_config, mix_seed, pack_pair, predict_sectors,
-    unpack_slot, value_for_key, values_for_keys,
+    reload_tuning, unpack_slot, value_for_key, values_for_keys,
 )
 from ._lib import Config  # noqa: E402
 from . import experiments, workload  # noqa: E402,F401

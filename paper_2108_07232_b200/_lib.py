@@ -100,6 +100,9 @@ SIGNATURES = {
     "bht_build": (C.c_int, [C.POINTER(Config), C.c_int32, _vp, _vp, C.c_uint64, C.c_int32, C.c_int32, C.POINTER(_vp),
                             C.POINTER(InsertResult), _vp]),
     "bht_insert_as": (C.c_int, [_vp, C.c_int32, _vp, _vp, C.c_uint64, C.c_int32, C.POINTER(InsertResult), _vp]),
+    "bht_build_begin": (C.c_int, [_vp, C.c_uint64, _vp]),
+    "bht_build_feed": (C.c_int, [_vp, _vp, _vp, C.c_uint64, _vp]),
+    "bht_build_end": (C.c_int, [_vp, C.POINTER(InsertResult), _vp]),
     "bht_find": (C.c_int, [_vp, _vp, _vp, C.c_uint64, C.c_int32, C.POINTER(FindResult), _vp]),
     "bht_find_as": (C.c_int, [_vp, C.c_int32, _vp, _vp, C.c_uint64, C.c_int32, C.POINTER(FindResult), _vp]),
     "bht_find_exhaustive": (C.c_int, [_vp, _vp, _vp, C.c_uint64, C.c_int32, C.POINTER(FindResult), _vp]),
@@ -139,6 +142,7 @@ SIGNATURES = {
     "bht_save_keys": (C.c_int, [C.c_char_p, _vp, C.c_uint64]),
     "bht_load_keys": (C.c_int, [C.c_char_p, _vp, C.c_uint64, _u64p]),
     "bht_version_string": (C.c_char_p, []),
+    "bht_reload_tuning": (None, []),
     "bht_kernel_launch_count": (C.c_uint64, []),
     "bht_sizeof_config": (C.c_size_t, []),
 }

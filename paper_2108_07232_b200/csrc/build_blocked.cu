@@ -54,6 +54,10 @@
 #define BHT_BUILD_TMA_STORE 1
 #endif
 
+#ifndef BHT_BUILD_PREFETCH  // 1: a CTA of K11 prefetches the bin of the CTA that will take its place into the L2
+#define BHT_BUILD_PREFETCH 1
+#endif
+
 #ifndef BHT_SPLIT_TMA  // 1: the next tile's input arrives by a bulk asynchronous copy (TMA) while this one is processed
 #define BHT_SPLIT_TMA 1
 #endif
@@ -163,7 +167,11 @@ __device__ __forceinline__ void split_tile_finish(SplitShared& s, const uint2 (&
     }
     if (lane == 31) s.warp_tot[warp] = x;
     // the reservation travels while the block meets at the barrier
+#if defined(BHT_EXP_NOGATOM)  // experiment (wrong results): the pass without its global reservations
+    if (h != 0 && threadIdx.x < n_dest) gbase = static_cast<uint32_t>(tile_id % 200u) * 24u;
+#else
     if (h != 0 && threadIdx.x < n_dest) gbase = atomicAdd(&cursor[dest_base + threadIdx.x], h);
+#endif
   }
   __syncthreads();
   if (kSplitBlock == 256 || threadIdx.x < 256) {
@@ -293,7 +301,12 @@ group_scatter_kernel(const __grid_constant__ GroupArgs a) {
     for (int j = 0; j < kSplitPerThread; ++j) {
       const uint32_t d = group_of(kv[j].x);
       uint32_t rank = 0;
+#if defined(BHT_EXP_NOATOMS)  // experiment (wrong results): the pass without its shared-memory ranking
+      rank = (threadIdx.x * 8 + j) & 15u;
+      if (threadIdx.x < 83 && j == 0) s.hist[threadIdx.x] = 24;
+#else
       if ((valid >> j) & 1u) rank = atomicAdd(&s.hist[d], 1u);
+#endif
       dr[j] = d | (rank << 8);
     }
     __syncthreads();  // every rank of the tile is taken, and `in` has been read by everyone
@@ -415,7 +428,7 @@ __device__ __forceinline__ uint32_t claim_unit(const uint4 v, uint32_t q, uint32
     const uint32_t k = e ? v.z : v.x, val = e ? v.w : v.y;
     if (!GUARD || 2u * q + e < n_r) {
       const uint32_t lb = bucket_index(h0, k) - first32;  // < nb: the bin holds pairs of this region only
-#if defined(BHT_EXP_NOSTORE) || defined(BHT_EXP_LINEAR)
+#if defined(BHT_EXP_NOSTORE) || defined(BHT_EXP_LINEAR) || defined(BHT_EXP_NOGATOM) || defined(BHT_EXP_NOATOMS)
       if (lb >= nb) continue;  // the experiments feed this kernel garbage
 #endif
       const uint32_t slot = atomicAdd(&cnt[lb], 1u);
@@ -549,7 +562,7 @@ region_build_kernel(const __grid_constant__ TableView t, uint32_t region_log2, u
       // a hole (only on an uploaded store): the pair is simply placed; the reserved list entry becomes a tombstone
       if (vk == kEmptyKey) atomicAdd(&hole_count, 1u);
       sp.pairs[stash_base + i] = make_uint2(vk, static_cast<uint32_t>(old >> 32));
-      sp.start[stash_base + i] = next | 0x80000000u;
+      sp.start[stash_base + i] = vk == kEmptyKey ? kStartTombstone : (next | 0x80000000u);
     }
   }
 #if BHT_BUILD_TMA_STORE
@@ -612,7 +625,7 @@ BlockedPlan plan_blocked_build(const TableView& t, uint64_t n) {
   if (region_bytes_log2 < 3 + b_log2 + 5) return p;
   const uint32_t region_log2 = region_bytes_log2 - 3 - b_log2;
   const uint64_t regions = (t.num_buckets + (1ull << region_log2) - 1) >> region_log2;
-  if (regions > 256ull * kMaxShards || t.num_buckets > 0x7FFFFFFFull) return p;  // two levels of <= 256 x 256; 31-bit start buckets
+  if (regions > 256ull * kMaxShards || t.num_buckets >= 0x7FFFFFFEull) return p;  // two levels of <= 256 x 256; 31-bit start buckets below the tombstone word
   uint32_t per = static_cast<uint32_t>(std::ceil(std::sqrt(static_cast<double>(regions))));
   if (per < 1) per = 1;
   if (per > 256) per = 256;
@@ -711,7 +724,7 @@ cudaError_t blocked_build_finish(const TableView& t, const BlockedPlan& p, uint6
   e = cudaFuncSetAttribute(region_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_c);
   if (e != cudaSuccess) return e;
   int per_sm = 0;
-#ifdef BHT_BUILD_PREFETCH  // measured (profiles/r02d_*): +200 MB of DRAM reads (the prefetched lines are fetched twice), no gain
+#if BHT_BUILD_PREFETCH
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, region_build_kernel, kBuildBlock, smem_c) != cudaSuccess) per_sm = 1;
 #endif
   region_build_kernel<<<p.n_regions, kBuildBlock, smem_c, stream>>>(t, p.region_log2, p.b_log2, p.cap, m.bin_cursor, m.bins,

@@ -61,6 +61,76 @@ struct DeviceScope {  // every call runs on the table's device and leaves the ca
   DeviceScope scope__(dev);      \
   if (scope__.err != cudaSuccess) return cuda_fail(scope__.err, "cudaSetDevice")
 
+// Tuning / experiment knobs from the environment, read ONCE per process (the first call that needs them), never on
+// the call path.  -1 / negative = not set.
+struct Knobs {
+  long stage_chunk_log2, insert_ctas, insert_grid, direct, sweep_mb, claim_insert, region_mb, smem_build, blocked_ctas,
+      tail_throttle, tail_div, chunk_log2;
+  double tail_lf;
+};
+long env_long(const char* name, long unset) {
+  const char* e = std::getenv(name);
+  return e != nullptr ? std::atol(e) : unset;
+}
+Knobs load_knobs() {
+  Knobs v;
+  v.stage_chunk_log2 = env_long("BHT_STAGE_CHUNK_LOG2", 22);  // 18..22
+  v.insert_ctas = env_long("BHT_INSERT_CTAS", -1);            // keys in flight (tools/exp_success_inflight.py)
+  v.insert_grid = env_long("BHT_INSERT_GRID", -1);
+  v.direct = env_long("BHT_DIRECT", 1);              // 0 = staged engine everywhere, 1 = direct engine (4 <= b <= 16), 2 = direct for routed builds only
+  v.sweep_mb = env_long("BHT_SWEEP_MB", 16);         // L2 prefetch distance of a routed build, 0 = off
+  v.claim_insert = env_long("BHT_CLAIM_INSERT", -1); // 0 = never, 1 = always the counter-claimed bp2ht / iht insert
+  v.region_mb = env_long("BHT_REGION_MB", 48);       // region size of the L2-routed build, 0 = off
+  v.smem_build = env_long("BHT_SMEM_BUILD", 1);      // 0: fall back to the L2-routed build
+  v.blocked_ctas = env_long("BHT_BLOCKED_CTAS", 0);  // resident CTAs per SM of a routed build's insert kernel, 0 = whatever fits
+  v.tail_throttle = env_long("BHT_TAIL_THROTTLE", -1);
+  v.tail_div = env_long("BHT_TAIL_DIV", 24);
+  v.chunk_log2 = env_long("BHT_CHUNK_LOG2", static_cast<long>(kDefaultChunkLog2));  // work-stream chunk (probe_engine.cuh, Stream)
+  const char* lf = std::getenv("BHT_TAIL_LF");
+  v.tail_lf = lf != nullptr ? std::atof(lf) : -1.0;
+  return v;
+}
+Knobs& knobs_storage() {
+  static Knobs k = load_knobs();
+  return k;
+}
+const Knobs& knobs() { return knobs_storage(); }
+
+// Stream-ordered scratch (routing / binning buffers, up to ~28 bytes per pair of a blocked build) comes from a pool the
+// library owns, one per device, kept cached while any table lives on the device and handed back to the driver when
+// the last one is destroyed — the process's default pool is left as the application configured it.
+struct ScratchPools {
+  std::mutex mu;
+  cudaMemPool_t pool[64] = {};
+  int users[64] = {};
+} g_pools;
+cudaMemPool_t scratch_pool(int device) { return device >= 0 && device < 64 ? g_pools.pool[device] : nullptr; }
+void scratch_pool_acquire(int device) {
+  if (device < 0 || device >= 64) return;
+  std::lock_guard<std::mutex> lock(g_pools.mu);
+  if (g_pools.pool[device] == nullptr) {
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.handleTypes = cudaMemHandleTypeNone;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = device;
+    cudaMemPool_t pool = nullptr;
+    if (cudaMemPoolCreate(&pool, &props) == cudaSuccess) {
+      unsigned long long keep = ~0ull;  // cached across calls; trimmed when the last table of the device goes
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+      g_pools.pool[device] = pool;
+    } else {
+      cudaGetLastError();  // fall back to the default pool (scratch_alloc)
+    }
+  }
+  ++g_pools.users[device];
+}
+void scratch_pool_release(int device) {
+  if (device < 0 || device >= 64) return;
+  std::lock_guard<std::mutex> lock(g_pools.mu);
+  if (--g_pools.users[device] == 0 && g_pools.pool[device] != nullptr) cudaMemPoolTrimTo(g_pools.pool[device], 0);
+}
+
 constexpr int kStageSlots = 3;
 constexpr uint64_t kStageChunk = 1ull << 22;  // keys per staged chunk: 16 MiB per array over PCIe (measured: 2^19..2^24 — 2^22 is the fastest)
 constexpr uint64_t kStageChunkMin = 1ull << 18;
@@ -69,11 +139,8 @@ constexpr uint64_t kStageChunkMin = 1ull << 18;
 // again towards the end, so the pipeline fills and drains in ~1 MiB steps (the first copy-in and the last
 // kernel / copy-out are the only parts of a host-buffer call that nothing overlaps).
 uint64_t stage_chunk_len(uint64_t off, uint64_t n) {
-  static const uint64_t chunk_max = [] {  // BHT_STAGE_CHUNK_LOG2: tuning knob, 18..22
-    const char* e = std::getenv("BHT_STAGE_CHUNK_LOG2");
-    const long v = e ? std::atol(e) : 22;
-    return 1ull << (v < 18 ? 18 : (v > 22 ? 22 : v));
-  }();
+  const long v = knobs().stage_chunk_log2;
+  const uint64_t chunk_max = 1ull << (v < 18 ? 18 : (v > 22 ? 22 : v));
   const uint64_t up = std::max(kStageChunkMin, off);
   const uint64_t down = std::max(kStageChunkMin, (n - off) / 2);
   return std::min(std::min(chunk_max, n - off), std::min(up, down));
@@ -113,6 +180,21 @@ struct bht_table {
   // build into an empty table writes every region of the store exactly once, empty slots included (K11), so the fill
   // is fused into it; every other use of the store calls materialize_clear first.
   std::atomic<bool> clear_pending{false};
+  // The deferred fill runs on the stream of whichever call pays the debt; calls on OTHER streams are ordered after it
+  // through this event for as long as it has not completed.
+  cudaEvent_t fill_done = nullptr;
+  cudaStream_t fill_stream = nullptr;
+  std::atomic<bool> fill_recorded{false};
+  cudaEvent_t build_done = nullptr;  // end of the device work of a host-buffer insert (which returns once the copies are in)
+  // bht_build_begin / _feed / _end: one build whose pairs arrive in chunks
+  struct Session {
+    bool active = false;
+    bool blocked = false;  // shared-memory-blocked build: chunks go through K8g, the rest happens at the end
+    BlockedPlan plan{};
+    void* scratch = nullptr;
+    uint64_t n_max = 0, fed = 0;
+    bool fresh = false;
+  } session;
   uint64_t host_inserted = 0;  // upper bound of the pairs in the store, kept on the host (tail_plan)
   bool tail_throttle = false;  // bht_set_tail_throttle
   // bp2ht / iht: one 32-bit load counter per bucket for the counter-claimed insert (insert_claim.cu); loads_valid =
@@ -235,28 +317,15 @@ cudaError_t launch_insert_kind(bht_table* t, PairSource src, uint64_t n, int max
   a.failed_cap = kFailedLogCap;
   a.sm_count = t->sm_count;
   a.max_ctas_per_sm = max_ctas_per_sm;
-  // experiment knobs on the number of keys in flight (tools/exp_success_inflight.py, DESIGN.md §3 K4)
-  if (const char* e = std::getenv("BHT_INSERT_CTAS")) {
-    const int v = std::atoi(e);
-    if (v > 0) a.max_ctas_per_sm = v;
-  }
-  a.max_grid = max_grid;
-  if (const char* e = std::getenv("BHT_INSERT_GRID")) a.max_grid = std::atoi(e);
-  {
-    // experiment knob: 0 = staged engine everywhere, 1 = direct engine everywhere (default: measured faster for
-    // 4 <= b <= 16 in caller order and in routed builds), 2 = direct for routed builds only
-    const char* e = std::getenv("BHT_DIRECT");
-    const int mode = e ? std::atoi(e) : 1;
-    a.direct = mode == 1 || (mode == 2 && routed);
-  }
+  const Knobs& k = knobs();
+  if (k.insert_ctas > 0) a.max_ctas_per_sm = static_cast<int>(k.insert_ctas);
+  a.max_grid = k.insert_grid >= 0 ? static_cast<int>(k.insert_grid) : max_grid;
+  // the direct engine is the default: measured faster for 4 <= b <= 16 in caller order and in routed builds
+  a.direct = k.direct == 1 || (k.direct == 2 && routed);
   a.stream = stream;
   cudaError_t e = next_cursor(t, stream, &a.work_cursor);
   if (e != cudaSuccess) return e;
-  {
-    const char* s = std::getenv("BHT_SWEEP_MB");  // tuning knob: L2 prefetch distance of a routed build, 0 = off
-    const long mb = s ? std::atol(s) : 16L;
-    t->view.sweep_ahead_bytes = static_cast<uint32_t>((mb < 0 ? 0 : (mb > 1024 ? 1024 : mb)) << 20);
-  }
+  t->view.sweep_ahead_bytes = static_cast<uint32_t>((k.sweep_mb < 0 ? 0 : (k.sweep_mb > 1024 ? 1024 : k.sweep_mb)) << 20);
   switch (t->cfg.kind) {
     case BHT_ONE_CHT:
     case BHT_BCHT:
@@ -268,8 +337,7 @@ cudaError_t launch_insert_kind(bht_table* t, PairSource src, uint64_t n, int max
       // Small tables keep the bucket-reading kernels (their probes are L2 hits anyway); whatever they write makes the
       // counters stale, and they are rebuilt from the store before the next counter-claimed launch.
       const bool big = t->cfg.capacity * sizeof(uint64_t) >= (192ull << 20);
-      const char* env = std::getenv("BHT_CLAIM_INSERT");  // experiment override: 0 = never, 1 = always
-      const bool claim = t->loads != nullptr && (env ? std::atoi(env) != 0 : (t->blocked_insert == 3 || (t->blocked_insert == 1 && big)));
+      const bool claim = t->loads != nullptr && (k.claim_insert >= 0 ? k.claim_insert != 0 : (t->blocked_insert == 3 || (t->blocked_insert == 1 && big)));
       if (claim) {
         if (!t->loads_valid) {
           e = launch_load_count(t->view, t->loads, t->sm_count, stream);
@@ -289,8 +357,7 @@ cudaError_t launch_insert_kind(bht_table* t, PairSource src, uint64_t n, int max
 // Worth it only when the store is well beyond the L2 and the batch is large enough to amortise the routing
 // pass.  BHT_REGION_MB (environment) overrides the region size; 0 disables blocking.
 uint32_t blocked_regions(const bht_table* t, uint64_t n) {
-  const char* env = std::getenv("BHT_REGION_MB");
-  const long region_mb = env ? std::atol(env) : 48L;
+  const long region_mb = knobs().region_mb;
   if (region_mb <= 0 || t->blocked_insert == 0 || n > 0x7FFFFFFFull) return 1;
   const uint64_t store_bytes = t->cfg.capacity * sizeof(uint64_t);
   const bool forced = t->blocked_insert >= 2;  // bht_set_blocked_insert(table, 2): route whatever the sizes (tests)
@@ -321,8 +388,7 @@ BlockedPlan smem_blocked_plan(const bht_table* t, uint64_t n) {
     // which at b = 1 shifts the probe means 1.6-3 % below the reference's interleaved process (2.0225 against 2.0554
     // probes per insert at LF 0.8) for a 4-9 % gain in time; at b = 16 the shift is 0.1 % and the gain 50 %.
     if (t->cfg.kind != BHT_BCHT) return none;
-    const char* env = std::getenv("BHT_SMEM_BUILD");  // 0: fall back to the L2-routed build
-    if (env != nullptr && std::atoi(env) == 0) return none;
+    if (knobs().smem_build == 0) return none;
     const uint64_t store_bytes = t->cfg.capacity * sizeof(uint64_t);
     // every region is read / written once whatever n: only for batches that are a sizeable part of the table
     if (n < (4ull << 20) || store_bytes < (192ull << 20) || n * 8 < t->cfg.capacity) return none;
@@ -334,8 +400,7 @@ BlockedPlan smem_blocked_plan(const bht_table* t, uint64_t n) {
 // flight per SM saturate the path, and fewer keys in flight mean fewer lost slot races inside the region.
 // BHT_BLOCKED_CTAS (environment) overrides; 0 = whatever fits.
 int blocked_ctas_per_sm() {
-  const char* e = std::getenv("BHT_BLOCKED_CTAS");
-  return e ? std::atoi(e) : 0;
+  return static_cast<int>(knobs().blocked_ctas);
 }
 
 // Optional (bht_set_tail_throttle): the last pairs of a cuckoo build that ends at a very high load are inserted with
@@ -358,20 +423,19 @@ TailPlan tail_plan(const bht_table* t, uint64_t n) {
   TailPlan p;
   if (t->cfg.kind != BHT_BCHT && t->cfg.kind != BHT_ONE_CHT) return p;
   bool on = t->tail_throttle;
-  if (const char* e = std::getenv("BHT_TAIL_THROTTLE")) on = std::atoi(e) != 0;  // experiment override
+  if (knobs().tail_throttle >= 0) on = knobs().tail_throttle != 0;  // experiment override
   if (!on) return p;
   const double cap = static_cast<double>(t->cfg.capacity);
   const uint32_t b = t->cfg.bucket_size;
   double lf = b == 1 ? 0.85 : (b == 2 ? 0.90 : (b == 4 ? 0.95 : 0.98));
-  if (const char* e = std::getenv("BHT_TAIL_LF")) lf = std::atof(e);
+  if (knobs().tail_lf > 0.0) lf = knobs().tail_lf;
   const uint64_t before = std::min<uint64_t>(t->host_inserted, t->cfg.capacity);
   const uint64_t after = std::min<uint64_t>(before + n, t->cfg.capacity);
   const uint64_t threshold = static_cast<uint64_t>(lf * cap);
   if (after <= threshold) return p;
   p.tail = std::min<uint64_t>(n, after - std::max(before, threshold));
   const uint64_t free_at_end = t->cfg.capacity - after;
-  uint64_t divisor = 24;
-  if (const char* e = std::getenv("BHT_TAIL_DIV")) divisor = std::max(1l, std::atol(e));  // tuning knob
+  const uint64_t divisor = static_cast<uint64_t>(std::max(1l, knobs().tail_div));
   const uint64_t lanes = std::max<uint64_t>(256, free_at_end / divisor);
   p.grid = static_cast<int>(std::min<uint64_t>((lanes + 255) / 256, 1u << 20));
   if (p.grid >= t->sm_count * 4) p = TailPlan{};  // no real throttle: one launch
@@ -388,11 +452,28 @@ bool defer_fill_pays(const bht_table* t) {
   return t->cfg.kind == BHT_BCHT && t->cfg.capacity * sizeof(uint64_t) >= (192ull << 20);
 }
 
-// Writes the empty pattern a deferred create / clear still owes (caller holds t->mu, or is the only user of t).
+// Orders `stream` after a deferred fill that another stream ran and that may still be in flight.
+cudaError_t order_after_fill(bht_table* t, cudaStream_t stream) {
+  if (!t->fill_recorded.load(std::memory_order_acquire)) return cudaSuccess;
+  if (cudaEventQuery(t->fill_done) == cudaSuccess) {  // long done: nothing to order against any more
+    t->fill_recorded.store(false, std::memory_order_release);
+    return cudaSuccess;
+  }
+  cudaGetLastError();  // cudaErrorNotReady is not an error
+  return stream == t->fill_stream ? cudaSuccess : cudaStreamWaitEvent(stream, t->fill_done, 0);
+}
+
+// Writes the empty pattern a deferred create / clear still owes (caller holds t->mu, or is the only user of t), and
+// orders `stream` after the fill when an earlier call ran it on another stream.
 cudaError_t materialize_clear(bht_table* t, cudaStream_t stream) {
-  if (!t->clear_pending.load(std::memory_order_acquire)) return cudaSuccess;
-  const cudaError_t e = launch_fill_empty(t->view.store, t->cfg.capacity, t->sm_count, stream);
-  if (e == cudaSuccess) t->clear_pending.store(false, std::memory_order_release);
+  if (!t->clear_pending.load(std::memory_order_acquire)) return order_after_fill(t, stream);
+  cudaError_t e = launch_fill_empty(t->view.store, t->cfg.capacity, t->sm_count, stream);
+  if (e == cudaSuccess) e = cudaEventRecord(t->fill_done, stream);
+  if (e == cudaSuccess) {
+    t->fill_stream = stream;
+    t->fill_recorded.store(true, std::memory_order_release);
+    t->clear_pending.store(false, std::memory_order_release);
+  }
   return e;
 }
 
@@ -403,6 +484,26 @@ bool kind_matches(int32_t table_kind, int32_t as_kind) {
   return table_kind == as_kind;
 }
 
+// Stream-ordered scratch from the library's own pool of the table's device (see scratch_pool).
+cudaError_t scratch_alloc(const bht_table* t, void** p, size_t bytes, cudaStream_t stream) {
+  cudaMemPool_t pool = scratch_pool(t->device);
+  return pool != nullptr ? cudaMallocFromPoolAsync(p, bytes, pool, stream) : cudaMallocAsync(p, bytes, stream);
+}
+
+// Finishes a shared-memory-blocked build whose pairs are all in the group segments: K10 + K11, then the general kernel
+// over the spill list (its length stays on the device).  The deferred fill is cancelled only once K11 is enqueued.
+cudaError_t finish_blocked(bht_table* t, const BlockedPlan& plan, uint64_t n, void* scratch, bool fresh, bool fused_fill,
+                           cudaStream_t stream) {
+  PairSource spill{};
+  const unsigned long long* spill_count = nullptr;
+  cudaError_t e = blocked_build_finish(t->view, plan, n, scratch, fresh, t->ctr, t->sm_count, stream, &spill, &spill_count);
+  if (e != cudaSuccess) return e;
+  if (fused_fill) t->clear_pending.store(false, std::memory_order_release);  // the region build writes every slot of the store
+  e = cudaEventRecord(t->phase_ev[1], stream);
+  if (e == cudaSuccess) e = launch_insert_kind(t, spill, n, 0, stream, false, spill_count);
+  return e;
+}
+
 bht_status do_insert(bht_table* t, const uint32_t* keys, const uint32_t* values, uint64_t n, int32_t mem_space,
                      bht_insert_result* result, void* stream_v) {
   if (t == nullptr) return fail(BHT_INVALID_ARGUMENT, "bht_insert: null table");
@@ -410,6 +511,7 @@ bht_status do_insert(bht_table* t, const uint32_t* keys, const uint32_t* values,
   if (mem_space != BHT_MEM_DEVICE && mem_space != BHT_MEM_HOST) return fail(BHT_INVALID_ARGUMENT, "bht_insert: bad mem_space");
   BHT_ON_DEVICE(t->device);
   std::lock_guard<std::mutex> lock(t->mu);
+  if (t->session.active) return fail(BHT_INVALID_ARGUMENT, "bht_insert: a chunked build (bht_build_begin) is open on this table");
   cudaStream_t stream = as_stream(stream_v);
   // values == NULL: the keys-only build of the reference, every key paired with value_for_key(key) (table.cpp:234).
   // Host callers then ship keys only; the values are made on the device.
@@ -418,8 +520,8 @@ bht_status do_insert(bht_table* t, const uint32_t* keys, const uint32_t* values,
     void* p = nullptr;
     cudaStream_t s = nullptr;
     ~AsyncBuffer() { if (p != nullptr) cudaFreeAsync(p, s); }
-  } derived;
-  derived.s = stream;
+  } derived, scratch;
+  derived.s = scratch.s = stream;
 
   BHT_CUDA(cudaMemsetAsync(t->ctr, 0, kPerCallCounterBytes, stream));
   const TailPlan tail = tail_plan(t, n);
@@ -429,13 +531,12 @@ bht_status do_insert(bht_table* t, const uint32_t* keys, const uint32_t* values,
     BHT_CUDA(cudaEventRecord(t->phase_ev[0], stream));
     const BlockedPlan plan = smem_blocked_plan(t, n);
     const uint32_t regions = plan.n_regions != 0 ? 1 : blocked_regions(t, n);
-    if (plan.n_regions != 0 && t->known_empty && n != 0)
-      t->clear_pending.store(false, std::memory_order_release);  // the region build writes every slot of the store
-    else
-      BHT_CUDA(materialize_clear(t, stream));
+    // a blocked build into the known-empty table writes every slot itself: the fill it still owes is fused into it
+    const bool fused_fill = plan.n_regions != 0 && t->known_empty && n != 0 && t->clear_pending.load(std::memory_order_acquire);
+    if (!fused_fill) BHT_CUDA(materialize_clear(t, stream));
     if (derive && n_all != 0 && (plan.n_regions == 0 || tail.tail != 0)) {
       // the shared-memory-blocked build makes the values in its first pass; every other schedule reads an array
-      BHT_CUDA(cudaMallocAsync(&derived.p, n_all * sizeof(uint32_t), stream));
+      BHT_CUDA(scratch_alloc(t, &derived.p, n_all * sizeof(uint32_t), stream));
       BHT_CUDA(launch_derive_values(keys, static_cast<uint32_t*>(derived.p), n_all, t->sm_count, stream));
       if (plan.n_regions == 0) values = static_cast<const uint32_t*>(derived.p);
     }
@@ -444,30 +545,24 @@ bht_status do_insert(bht_table* t, const uint32_t* keys, const uint32_t* values,
       // Shared-memory-blocked build (build_blocked.cu): bin the pairs by the shared-memory-sized table region of
       // their first bucket, build every region in shared memory, then run the general kernel over the pairs whose
       // first bucket was full (their count stays on the device).
-      void* scratch = nullptr;
-      BHT_CUDA(cudaMallocAsync(&scratch, blocked_scratch_bytes(plan, n), stream));
-      PairSource spill{};
-      const unsigned long long* spill_count = nullptr;
-      cudaError_t e = launch_blocked_build(t->view, plan, keys, values, n, t->known_empty, scratch, t->ctr, t->sm_count, stream,
-                                           &spill, &spill_count);
-      if (e == cudaSuccess) e = cudaEventRecord(t->phase_ev[1], stream);
-      if (e == cudaSuccess)
-        e = launch_insert_kind(t, spill, n, 0, stream, false, spill_count);
-      cudaFreeAsync(scratch, stream);
+      BHT_CUDA(scratch_alloc(t, &scratch.p, blocked_scratch_bytes(plan, n), stream));
+      cudaError_t e = blocked_build_begin(plan, n, scratch.p, stream);
+      if (e == cudaSuccess) e = blocked_build_scatter(t->view, plan, n, scratch.p, keys, values, n, t->sm_count, stream);
+      if (e == cudaSuccess) e = finish_blocked(t, plan, n, scratch.p, t->known_empty, fused_fill, stream);
       if (e != cudaSuccess) return cuda_fail(e, "bht_insert (shared-memory blocked)");
     } else if (regions > 1) {
       // L2-blocked build: group the pairs by the table region of their first bucket, then insert region by
       // region, so that bucket fetches, claims and the write-back of dirty sectors happen while the region
       // is L2-resident (the probe kernels deal their input out as one sliding window, probe_engine.cuh).
-      uint32_t* scratch = nullptr;  // n packed {key, value} pairs | counts | cursors | n destination bytes
-      BHT_CUDA(cudaMallocAsync(&scratch, 2 * n * sizeof(uint32_t) + 2 * regions * sizeof(unsigned long long) + n, stream));
-      unsigned long long* counts = reinterpret_cast<unsigned long long*>(scratch + 2 * n);
+      // scratch: n packed {key, value} pairs | counts | cursors | n destination bytes
+      BHT_CUDA(scratch_alloc(t, &scratch.p, 2 * n * sizeof(uint32_t) + 2 * regions * sizeof(unsigned long long) + n, stream));
+      uint32_t* packed = static_cast<uint32_t*>(scratch.p);
+      unsigned long long* counts = reinterpret_cast<unsigned long long*>(packed + 2 * n);
       uint8_t* dest8 = reinterpret_cast<uint8_t*>(counts + 2 * regions);
-      cudaError_t e = launch_region_route(t->view.h[0], regions, keys, values, n, dest8, counts, counts + regions, scratch,
+      cudaError_t e = launch_region_route(t->view.h[0], regions, keys, values, n, dest8, counts, counts + regions, packed,
                                           t->sm_count, stream);
       if (e == cudaSuccess) e = cudaEventRecord(t->phase_ev[1], stream);
-      if (e == cudaSuccess) e = launch_insert_kind(t, PairSource{scratch, nullptr}, n, blocked_ctas_per_sm(), stream, true);
-      cudaFreeAsync(scratch, stream);
+      if (e == cudaSuccess) e = launch_insert_kind(t, PairSource{packed, nullptr}, n, blocked_ctas_per_sm(), stream, true);
       if (e != cudaSuccess) return cuda_fail(e, "bht_insert (blocked)");
     } else {
       BHT_CUDA(cudaEventRecord(t->phase_ev[1], stream));
@@ -478,34 +573,58 @@ bht_status do_insert(bht_table* t, const uint32_t* keys, const uint32_t* values,
     BHT_CUDA(cudaEventRecord(t->phase_ev[2], stream));
     t->phases_recorded = true;
   } else if (n_all != 0) {
+    // Host-resident arrays: chunks cross PCIe through the staging slots while the device works on the chunks that have
+    // arrived.  A batch that qualifies for the shared-memory-blocked build feeds every chunk to its first partition
+    // pass (K8g) as it lands and runs the rest (K10, K11, the walks) once the last chunk is in; everything else goes
+    // through the general kernel chunk by chunk.  The call returns when the caller's arrays have been read; the device
+    // work still in flight is ordered before anything enqueued later on `stream` or done later with this table.
     n = n_all;
     const uint64_t n_main = n_all - tail.tail;
     bht_status s = ensure_staging(t);
     if (s != BHT_OK) return s;
-    BHT_CUDA(materialize_clear(t, stream));
     Staging& st = t->stage;
+    const BlockedPlan plan = tail.tail == 0 ? smem_blocked_plan(t, n) : BlockedPlan{};
+    const bool blocked = plan.n_regions != 0;
+    const bool fused_fill = blocked && t->known_empty && t->clear_pending.load(std::memory_order_acquire);
+    if (!fused_fill) BHT_CUDA(materialize_clear(t, stream));
     cudaEvent_t start = st.out_done[0];  // reuse as the "counters are zeroed" marker
     BHT_CUDA(cudaEventRecord(start, stream));
     BHT_CUDA(cudaStreamWaitEvent(st.compute, start, 0));
+    scratch.s = st.compute;
+    if (blocked) {
+      BHT_CUDA(scratch_alloc(t, &scratch.p, blocked_scratch_bytes(plan, n), st.compute));
+      BHT_CUDA(blocked_build_begin(plan, n, scratch.p, st.compute));
+    }
     uint64_t chunks = 0;
     for (uint64_t c = 0, off = 0; off < n; ++c) {
       const int slot = static_cast<int>(c % kStageSlots);
       uint64_t len = stage_chunk_len(off, n);
       if (off < n_main) len = std::min(len, n_main - off);  // a chunk is either before or inside the throttled tail
       chunks = c + 1;
-      if (c >= kStageSlots) BHT_CUDA(cudaStreamWaitEvent(st.h2d, st.kernel_done[slot], 0));
+      // the slot's last consumer — of this call or of an earlier one whose device work is still in flight — is done
+      BHT_CUDA(cudaStreamWaitEvent(st.h2d, st.kernel_done[slot], 0));
       BHT_CUDA(cudaMemcpyAsync(st.keys[slot], keys + off, len * sizeof(uint32_t), cudaMemcpyHostToDevice, st.h2d));
       if (!derive) BHT_CUDA(cudaMemcpyAsync(st.vals[slot], values + off, len * sizeof(uint32_t), cudaMemcpyHostToDevice, st.h2d));
       BHT_CUDA(cudaEventRecord(st.in_done[slot], st.h2d));
       BHT_CUDA(cudaStreamWaitEvent(st.compute, st.in_done[slot], 0));
-      if (derive) BHT_CUDA(launch_derive_values(st.keys[slot], st.vals[slot], len, t->sm_count, st.compute));
-      BHT_CUDA(launch_insert_kind(t, PairSource{st.keys[slot], st.vals[slot]}, len, 0, st.compute, false, nullptr,
-                                  off >= n_main ? tail.grid : 0));
+      if (blocked) {
+        BHT_CUDA(blocked_build_scatter(t->view, plan, n, scratch.p, st.keys[slot], derive ? nullptr : st.vals[slot], len,
+                                       t->sm_count, st.compute));
+      } else {
+        if (derive) BHT_CUDA(launch_derive_values(st.keys[slot], st.vals[slot], len, t->sm_count, st.compute));
+        BHT_CUDA(launch_insert_kind(t, PairSource{st.keys[slot], st.vals[slot]}, len, 0, st.compute, false, nullptr,
+                                    off >= n_main ? tail.grid : 0));
+      }
       BHT_CUDA(cudaEventRecord(st.kernel_done[slot], st.compute));
       off += len;
     }
-    BHT_CUDA(cudaStreamWaitEvent(stream, st.kernel_done[(chunks - 1) % kStageSlots], 0));
-    BHT_CUDA(cudaStreamSynchronize(stream));  // the caller's host arrays are free again on return
+    if (blocked) {
+      const cudaError_t e = finish_blocked(t, plan, n, scratch.p, t->known_empty, fused_fill, st.compute);
+      if (e != cudaSuccess) return cuda_fail(e, "bht_insert (host buffers, shared-memory blocked)");
+    }
+    BHT_CUDA(cudaEventRecord(t->build_done, st.compute));
+    BHT_CUDA(cudaStreamWaitEvent(stream, t->build_done, 0));
+    BHT_CUDA(cudaEventSynchronize(st.in_done[(chunks - 1) % kStageSlots]));  // the caller's host arrays are free again on return
   }
   n = n_all;
   if (n != 0) t->known_empty = false;
@@ -514,6 +633,99 @@ bht_status do_insert(bht_table* t, const uint32_t* keys, const uint32_t* values,
     bht_status s = read_counters(t, stream);
     if (s != BHT_OK) return s;
     fill_insert_result(t, n, result);
+  }
+  return BHT_OK;
+}
+
+// ---- a build whose pairs arrive in chunks (device-resident): bht_build_begin / _feed / _end ----------------------
+bht_status session_begin(bht_table* t, uint64_t n_max, void* stream_v) {
+  if (t == nullptr) return fail(BHT_INVALID_ARGUMENT, "bht_build_begin: null table");
+  BHT_ON_DEVICE(t->device);
+  std::lock_guard<std::mutex> lock(t->mu);
+  if (t->session.active) return fail(BHT_INVALID_ARGUMENT, "bht_build_begin: a chunked build is already open on this table");
+  cudaStream_t stream = as_stream(stream_v);
+  bht_table::Session ses;
+  ses.n_max = n_max;
+  ses.fresh = t->known_empty;
+  BHT_CUDA(cudaMemsetAsync(t->ctr, 0, kPerCallCounterBytes, stream));
+  BHT_CUDA(cudaEventRecord(t->phase_ev[0], stream));
+  ses.plan = n_max != 0 ? smem_blocked_plan(t, n_max) : BlockedPlan{};
+  ses.blocked = ses.plan.n_regions != 0;
+  if (ses.blocked) {
+    BHT_CUDA(scratch_alloc(t, &ses.scratch, blocked_scratch_bytes(ses.plan, n_max), stream));
+    const cudaError_t e = blocked_build_begin(ses.plan, n_max, ses.scratch, stream);
+    if (e != cudaSuccess) {
+      cudaFreeAsync(ses.scratch, stream);
+      return cuda_fail(e, "bht_build_begin");
+    }
+  }
+  ses.active = true;
+  t->session = ses;
+  return BHT_OK;
+}
+
+bht_status session_feed(bht_table* t, const uint32_t* keys, const uint32_t* values, uint64_t n, void* stream_v) {
+  if (t == nullptr) return fail(BHT_INVALID_ARGUMENT, "bht_build_feed: null table");
+  if (n != 0 && keys == nullptr) return fail(BHT_INVALID_ARGUMENT, "bht_build_feed: null keys");
+  BHT_ON_DEVICE(t->device);
+  std::lock_guard<std::mutex> lock(t->mu);
+  bht_table::Session& ses = t->session;
+  if (!ses.active) return fail(BHT_INVALID_ARGUMENT, "bht_build_feed: no chunked build is open (bht_build_begin)");
+  if (ses.fed + n > ses.n_max) return fail(BHT_CAPACITY_EXCEEDED, "bht_build_feed: more pairs than bht_build_begin announced");
+  cudaStream_t stream = as_stream(stream_v);
+  if (n == 0) return BHT_OK;
+  if (ses.blocked) {
+    BHT_CUDA(blocked_build_scatter(t->view, ses.plan, ses.n_max, ses.scratch, keys, values, n, t->sm_count, stream));
+  } else {
+    BHT_CUDA(materialize_clear(t, stream));
+    void* derived = nullptr;
+    if (values == nullptr) {
+      BHT_CUDA(scratch_alloc(t, &derived, n * sizeof(uint32_t), stream));
+      const cudaError_t e = launch_derive_values(keys, static_cast<uint32_t*>(derived), n, t->sm_count, stream);
+      if (e != cudaSuccess) {
+        cudaFreeAsync(derived, stream);
+        return cuda_fail(e, "bht_build_feed");
+      }
+      values = static_cast<const uint32_t*>(derived);
+    }
+    const cudaError_t e = launch_insert_kind(t, PairSource{keys, values}, n, 0, stream);
+    if (derived != nullptr) cudaFreeAsync(derived, stream);
+    if (e != cudaSuccess) return cuda_fail(e, "bht_build_feed");
+    t->known_empty = false;
+  }
+  ses.fed += n;
+  return BHT_OK;
+}
+
+bht_status session_end(bht_table* t, bht_insert_result* result, void* stream_v) {
+  if (t == nullptr) return fail(BHT_INVALID_ARGUMENT, "bht_build_end: null table");
+  BHT_ON_DEVICE(t->device);
+  std::lock_guard<std::mutex> lock(t->mu);
+  bht_table::Session& ses = t->session;
+  if (!ses.active) return fail(BHT_INVALID_ARGUMENT, "bht_build_end: no chunked build is open (bht_build_begin)");
+  cudaStream_t stream = as_stream(stream_v);
+  cudaError_t e = cudaSuccess;
+  if (ses.blocked) {
+    if (ses.fed != 0) {
+      const bool fused_fill = ses.fresh && t->known_empty && t->clear_pending.load(std::memory_order_acquire);
+      if (!fused_fill) e = materialize_clear(t, stream);
+      if (e == cudaSuccess) e = finish_blocked(t, ses.plan, ses.n_max, ses.scratch, ses.fresh && t->known_empty, fused_fill, stream);
+    }
+    cudaFreeAsync(ses.scratch, stream);
+  } else {
+    e = cudaEventRecord(t->phase_ev[1], stream);
+  }
+  const uint64_t fed = ses.fed;
+  ses = bht_table::Session{};
+  if (e != cudaSuccess) return cuda_fail(e, "bht_build_end");
+  BHT_CUDA(cudaEventRecord(t->phase_ev[2], stream));
+  t->phases_recorded = true;
+  if (fed != 0) t->known_empty = false;
+  t->host_inserted = std::min<uint64_t>(t->host_inserted + fed, t->cfg.capacity);
+  if (result != nullptr) {
+    const bht_status s = read_counters(t, stream);
+    if (s != BHT_OK) return s;
+    fill_insert_result(t, fed, result);
   }
   return BHT_OK;
 }
@@ -530,6 +742,8 @@ bht_status do_find(const bht_table* ct, bool early_exit, const uint32_t* keys, u
   if (t->clear_pending.load(std::memory_order_acquire)) {
     std::lock_guard<std::mutex> lock(t->mu);
     BHT_CUDA(materialize_clear(t, stream));
+  } else {
+    BHT_CUDA(order_after_fill(t, stream));
   }
   if (mem_space == BHT_MEM_DEVICE && result == nullptr) {
     // lock-free: concurrent finds on different streams share nothing but the read-only store
@@ -559,10 +773,9 @@ bht_status do_find(const bht_table* ct, bool early_exit, const uint32_t* keys, u
       const int slot = static_cast<int>(c % kStageSlots);
       const uint64_t len = stage_chunk_len(off, n);
       chunks = c + 1;
-      if (c >= kStageSlots) {
-        BHT_CUDA(cudaStreamWaitEvent(st.h2d, st.kernel_done[slot], 0));   // keys[slot] consumed
-        BHT_CUDA(cudaStreamWaitEvent(st.compute, st.out_done[slot], 0));  // vals[slot] drained
-      }
+      // (also against the kernels of an earlier host-buffer insert, which returns before its device work is done)
+      BHT_CUDA(cudaStreamWaitEvent(st.h2d, st.kernel_done[slot], 0));                       // keys[slot] consumed
+      if (c >= kStageSlots) BHT_CUDA(cudaStreamWaitEvent(st.compute, st.out_done[slot], 0));  // vals[slot] drained
       BHT_CUDA(cudaMemcpyAsync(st.keys[slot], keys + off, len * sizeof(uint32_t), cudaMemcpyHostToDevice, st.h2d));
       BHT_CUDA(cudaEventRecord(st.in_done[slot], st.h2d));
       BHT_CUDA(cudaStreamWaitEvent(st.compute, st.in_done[slot], 0));
@@ -693,15 +906,7 @@ bht_status bht_create(const bht_config* cfg, int32_t device, bht_table** out) {
     return fail(BHT_CUDA_ERROR, "bht_create: kernels are built for sm_100a only; this device is older");
   }
   if (e == cudaSuccess) t->sm_count = prop.multiProcessorCount;
-  {
-    // scratch for routed inserts comes from the stream-ordered pool: keep it cached across calls instead of
-    // handing it back to the driver at every synchronisation
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
-      unsigned long long keep = ~0ull;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-    }
-  }
+  scratch_pool_acquire(device);
 
   uint64_t* store = nullptr;
   if (e == cudaSuccess) e = cudaMalloc(&store, cfg->capacity * sizeof(uint64_t));  // cudaMalloc aligns to >= 256 B
@@ -710,6 +915,8 @@ bht_status bht_create(const bht_config* cfg, int32_t device, bht_table** out) {
   if (e == cudaSuccess) e = cudaMalloc(&t->failed_keys, kFailedLogCap * sizeof(uint32_t));
   if (e == cudaSuccess) e = cudaMalloc(&t->cursors, kCursorSlots * sizeof(uint32_t));
   for (int i = 0; i < 3 && e == cudaSuccess; ++i) e = cudaEventCreate(&t->phase_ev[i]);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&t->fill_done, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&t->build_done, cudaEventDisableTiming);
   if (e == cudaSuccess && (cfg->kind == BHT_BP2HT || cfg->kind == BHT_IHT)) {
     e = cudaMalloc(&t->loads, claim_loads_bytes(cfg->num_buckets));
     if (e == cudaSuccess) e = cudaMemset(t->loads, 0, claim_loads_bytes(cfg->num_buckets));
@@ -726,6 +933,12 @@ bht_status bht_create(const bht_config* cfg, int32_t device, bht_table** out) {
     if (t->ctr_host) cudaFreeHost(t->ctr_host);
     if (t->failed_keys) cudaFree(t->failed_keys);
     if (t->cursors) cudaFree(t->cursors);
+    if (t->loads) cudaFree(t->loads);
+    for (cudaEvent_t ev : t->phase_ev)
+      if (ev) cudaEventDestroy(ev);
+    if (t->fill_done) cudaEventDestroy(t->fill_done);
+    if (t->build_done) cudaEventDestroy(t->build_done);
+    scratch_pool_release(device);
     delete t;
     return cuda_fail(e, "bht_create");
   }
@@ -743,8 +956,7 @@ bht_status bht_create(const bht_config* cfg, int32_t device, bht_table** out) {
   v.prose = 0;
   v.retry_cap = kRetryCap;
   {
-    const char* e = std::getenv("BHT_CHUNK_LOG2");  // tuning knob: work-stream chunk (probe_engine.cuh, Stream)
-    const long c = e ? std::atol(e) : static_cast<long>(kDefaultChunkLog2);
+    const long c = knobs().chunk_log2;
     v.chunk_log2 = static_cast<uint32_t>(c < 5 ? 5 : (c > 16 ? 16 : c));
   }
   *out = t;
@@ -764,6 +976,10 @@ bht_status bht_destroy(bht_table* t) {
   if (t->loads) cudaFree(t->loads);
   for (cudaEvent_t ev : t->phase_ev)
     if (ev) cudaEventDestroy(ev);
+  if (t->session.active && t->session.scratch != nullptr) cudaFree(t->session.scratch);
+  if (t->fill_done) cudaEventDestroy(t->fill_done);
+  if (t->build_done) cudaEventDestroy(t->build_done);
+  scratch_pool_release(t->device);
   delete t;
   return BHT_OK;
 }
@@ -772,6 +988,7 @@ bht_status bht_clear(bht_table* t, void* stream) {
   if (t == nullptr) return fail(BHT_INVALID_ARGUMENT, "bht_clear: null table");
   BHT_ON_DEVICE(t->device);
   std::lock_guard<std::mutex> lock(t->mu);
+  if (t->session.active) return fail(BHT_INVALID_ARGUMENT, "bht_clear: a chunked build (bht_build_begin) is open on this table");
   if (defer_fill_pays(t)) {
     t->clear_pending.store(true, std::memory_order_release);  // deferred, see bht_table::clear_pending
   } else {
@@ -821,6 +1038,12 @@ bht_status bht_build(const bht_config* cfg, int32_t device, const uint32_t* keys
   *out = t;
   return BHT_OK;
 }
+
+bht_status bht_build_begin(bht_table* t, uint64_t n_max, void* stream) { return session_begin(t, n_max, stream); }
+bht_status bht_build_feed(bht_table* t, const uint32_t* keys, const uint32_t* values, uint64_t n, void* stream) {
+  return session_feed(t, keys, values, n, stream);
+}
+bht_status bht_build_end(bht_table* t, bht_insert_result* result, void* stream) { return session_end(t, result, stream); }
 
 bht_status bht_insert_as(bht_table* t, int32_t kind, const uint32_t* keys, const uint32_t* values, uint64_t n,
                          int32_t mem_space, bht_insert_result* result, void* stream) {
@@ -1122,6 +1345,7 @@ bht_status bht_host_free(void* p) {
 
 // ---- diagnostics -------------------------------------------------------------------------------------
 
+void bht_reload_tuning(void) { knobs_storage() = load_knobs(); }
 const char* bht_last_error_string(void) { return g_error.c_str(); }
 const char* bht_version_string(void) { return "bht_b200 0.1 (sm_100a)"; }
 uint64_t bht_kernel_launch_count(void) { return launch_count(); }

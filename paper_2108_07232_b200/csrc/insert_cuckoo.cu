@@ -75,7 +75,7 @@ bulk_insert_cuckoo_kernel(const __grid_constant__ TableView t, const PairSource 
       // on where build_blocked.cu left it
       bid = start == kStartAtH0 ? bucket_index(t.h[0], key) : (start & 0x7FFFFFFFu);
       chain = start == kStartAtH0 ? 0u : (start >> 31);
-      if (src.start != nullptr && key == kEmptyKey) have = false;  // tombstone of the blocked build (a hole was filled)
+      if (start == kStartTombstone) have = false;  // the blocked build filled a hole: the list entry holds no pair
       retries = 0;
       hint = kNoHint;
     }
@@ -106,7 +106,7 @@ bulk_insert_cuckoo_kernel(const __grid_constant__ TableView t, const PairSource 
     // Decide first, then issue the lane's one atomic, then look at the results: the claims (CAS) and the
     // evictions (EXCH) of a round are all in flight together instead of one divergent path after the other.
     const bool claim = have && !sitting && load < B;
-    const bool dropped = have && !sitting && !claim && chain == t.max_chain;  // cap checked BEFORE the exchange (table.cpp:67)
+    const bool dropped = have && !sitting && !claim && chain >= t.max_chain;  // cap checked BEFORE the exchange (table.cpp:67)
     const bool evict = have && !sitting && !claim && !dropped;
     const uint32_t slot = claim ? load : xorshift_next_below_if(rng, B, evict);
     unsigned long long* target = store + static_cast<uint64_t>(bid) * B + slot;

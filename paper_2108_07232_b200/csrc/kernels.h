@@ -23,6 +23,7 @@ struct PairSource {
   const uint32_t* start = nullptr;
 };
 constexpr uint32_t kStartAtH0 = 0xFFFFFFFFu;
+constexpr uint32_t kStartTombstone = 0xFFFFFFFEu;  // a reserved list entry that holds no pair (the blocked build filled a hole)
 
 struct InsertLaunch {
   PairSource src;
@@ -45,14 +46,14 @@ cudaError_t launch_insert_cuckoo(const TableView& t, const InsertLaunch& a);
 cudaError_t launch_insert_p2(const TableView& t, const InsertLaunch& a);
 cudaError_t launch_insert_iht(const TableView& t, const InsertLaunch& a);
 
-// insert_claim.cu — K12 (bp2ht) / K13 (iht): counter-claimed insert.  `loads`: one 16-bit load counter per bucket
+// insert_claim.cu — K12 (bp2ht) / K13 (iht): counter-claimed insert.  `loads`: one 32-bit load counter per bucket
 // (claim_loads_bytes), exact for the store (zero for an empty one, else rebuilt by launch_load_count).
 size_t claim_loads_bytes(uint64_t num_buckets);
 cudaError_t launch_load_count(const TableView& t, uint32_t* loads, int sm_count, cudaStream_t stream);
 cudaError_t launch_claim_insert(const TableView& t, uint32_t* loads, const InsertLaunch& a, bool iht);
 
-// build_blocked.cu — K10 bin_scatter + K11 region_build: the shared-memory-blocked first pass of a cuckoo build.
-constexpr uint32_t kMaxBlockedRegions = 40000;  // 16-bit region ids, histogram of one tile in shared memory
+// build_blocked.cu — K8g group_scatter + K10 bin_split + K11 region_build: the shared-memory-blocked first pass of a
+// cuckoo build.
 struct BlockedPlan {
   uint32_t n_regions;    // fine regions (one CTA of K11 each); 0: the blocked build does not apply
   uint32_t region_log2;  // buckets per fine region (64 KiB of slots)
@@ -70,6 +71,14 @@ size_t blocked_scratch_bytes(const BlockedPlan& p, uint64_t n);
 cudaError_t launch_blocked_build(const TableView& t, const BlockedPlan& p, const uint32_t* keys, const uint32_t* values,
                                  uint64_t n, bool fresh, void* scratch, DevCounters* ctr, int sm_count, cudaStream_t stream,
                                  PairSource* spill_out, const unsigned long long** spill_count_out);
+// The same build in steps, for a batch that arrives in chunks (n = the most pairs the chunks may add up to, the value
+// the plan and the scratch were sized for): begin, then scatter once per chunk (K8g), then finish (K10 + K11).
+cudaError_t blocked_build_begin(const BlockedPlan& p, uint64_t n, void* scratch, cudaStream_t stream);
+cudaError_t blocked_build_scatter(const TableView& t, const BlockedPlan& p, uint64_t n, void* scratch, const uint32_t* keys,
+                                  const uint32_t* values, uint64_t len, int sm_count, cudaStream_t stream);
+cudaError_t blocked_build_finish(const TableView& t, const BlockedPlan& p, uint64_t n, void* scratch, bool fresh,
+                                 DevCounters* ctr, int sm_count, cudaStream_t stream, PairSource* spill_out,
+                                 const unsigned long long** spill_count_out);
 
 // util.cu — K0 fill, K7 count, admissibility, hash hook, K8/K9 shard routing, synthetic keys.
 cudaError_t launch_fill_empty(uint64_t* store, uint64_t n_slots, int sm_count, cudaStream_t stream);

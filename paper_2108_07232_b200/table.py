@@ -341,6 +341,34 @@ class HashTable:
         return BuildOutcome(bool(res.success), res.inserted, res.failed, res.attempted, res.probes,
                             None if res.first_failed_key == EMPTY_KEY else res.first_failed_key)
 
+    # -- a build whose pairs arrive in chunks (bht_build_begin / _feed / _end)
+    def build_begin(self, n_max: int, stream=None) -> None:
+        """Opens a chunked build of at most ``n_max`` pairs (the receive side of a sharded build)."""
+        _check(self._lib.bht_build_begin(self._h, int(n_max), _stream_ptr(stream, self.device)))
+
+    def build_feed(self, keys, values=None, n: Optional[int] = None, stream=None) -> None:
+        """Adds a device-resident chunk; ``values=None`` pairs every key with value_for_key(key)."""
+        kp, kn, kspace, _k = _as_u32(keys, "keys")
+        if kspace != _lib.MEM_DEVICE:
+            raise ValueError("build_feed: chunks must be device-resident")
+        vp = None
+        n = kn if n is None else int(n)
+        if values is not None:
+            vp, vn, vspace, _v = _as_u32(values, "values")
+            if vspace != _lib.MEM_DEVICE or vn < n:
+                raise ValueError("build_feed: values must be device-resident and at least n long")
+        if n > kn:
+            raise ValueError("build_feed: n exceeds the array length")
+        _check(self._lib.bht_build_feed(self._h, kp, vp, n, _stream_ptr(stream, self.device)))
+
+    def build_end(self, stream=None, want_result: bool = True) -> Optional[BuildOutcome]:
+        res = InsertResult()
+        _check(self._lib.bht_build_end(self._h, C.byref(res) if want_result else None, _stream_ptr(stream, self.device)))
+        if not want_result:
+            return None
+        return BuildOutcome(bool(res.success), res.inserted, res.failed, res.attempted, res.probes,
+                            None if res.first_failed_key == EMPTY_KEY else res.first_failed_key)
+
     def last_insert_result(self, stream=None) -> BuildOutcome:
         res = InsertResult()
         _check(self._lib.bht_last_insert_result(self._h, C.byref(res), _stream_ptr(stream, self.device)))
@@ -492,6 +520,11 @@ def generate_unique_keys(seed: int, offset: int, n: int, device: Optional[int] =
     _check(lib.bht_generate_unique_keys(seed, offset, n, keys.data_ptr(), vals.data_ptr() if with_values else None,
                                         device, _stream_ptr(stream, device)))
     return (keys, vals) if with_values else keys
+
+
+def reload_tuning() -> None:
+    """Re-reads the BHT_* tuning environment variables (the library reads them once per process)."""
+    _lib.load().bht_reload_tuning()
 
 
 def kernel_launch_count() -> int:

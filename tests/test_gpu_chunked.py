@@ -1,0 +1,192 @@
+"""Chunked builds (bht_build_begin / _feed / _end), host-buffer builds through the blocked pipeline, the chain cap of
+zero, and the ordering of a deferred fill across streams — checked like every other build: stored multiset, the
+oracle's admissibility check and the oracle's answers on the GPU-built layout."""
+import numpy as np
+import pytest
+
+from conftest import random_values, to_oracle_cfg, unique_keys
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+EMPTY = 0xFFFFFFFF
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a).view(np.int32)).cuda()
+
+
+def host(t):
+    return t.cpu().numpy().view(np.uint32)
+
+
+def packed(keys, values):
+    return np.sort((values.astype(np.uint64) << np.uint64(32)) | keys.astype(np.uint64))
+
+
+def stored(table):
+    s = table.download_store()
+    return np.sort(s[s != np.uint64(0xFFFFFFFFFFFFFFFF)])
+
+
+CELLS = [("bcht", 16, 0.9, None, 3), ("bcht", 16, 0.9, None, 1), ("bcht", 8, 0.85, None, 3), ("bcht", 32, 0.9, None, 3),
+         ("1cht", 1, 0.7, None, 3), ("1cht", 1, 0.7, None, 1), ("bp2ht", 16, 0.75, None, 1), ("bp2ht", 16, 0.75, None, 3),
+         ("iht", 16, 0.8, 12, 3), ("iht", 16, 0.8, 12, 0)]
+
+
+@pytest.mark.parametrize("kind,b,lf,t,mode", CELLS)
+@pytest.mark.parametrize("with_values", [True, False])
+def test_chunked_build_equals_one_bulk_insert(bht, ora, kind, b, lf, t, mode, with_values):
+    """build() with the key set handed over in ragged chunks (table.cpp:231-271): same stored multiset, admissible,
+    same answers and the same aggregate outcome as one bulk insert; empty chunks and an unaligned chunk included."""
+    n = 220_007
+    keys = unique_keys(n, 4100 + b, extra=3000)
+    present, absent = keys[:n], keys[n:]
+    values = random_values(n, 17 * b) if with_values else ora.values_for_keys(present)
+    extra = {"threshold": t} if t is not None else {}
+    cfg = bht.make_config(kind, n, lf, b, seed=bht.mix_seed(77, b), **extra)
+    table = bht.HashTable(cfg, 0)
+    table.set_blocked_insert(mode)
+    d_keys, d_vals = dev(present), dev(values)
+    cuts = [0, 1, 1, 4097, 70_001, 70_004, 150_000, n]
+    table.build_begin(n)
+    with pytest.raises(ValueError):
+        table.insert(d_keys[:4], d_vals[:4])  # no plain insert while a chunked build is open
+    for lo, hi in zip(cuts[:-1], cuts[1:]):
+        table.build_feed(d_keys[lo:hi], d_vals[lo:hi] if with_values else None)
+    with pytest.raises(bht.CapacityError):
+        table.build_feed(d_keys[:1], d_vals[:1] if with_values else None)  # more than announced
+    o = table.build_end()
+    assert o.success and o.inserted == n and o.attempted == n and o.failed == 0
+    assert table.inserted() == n == table.occupied_slots() and table.count_inadmissible() == 0
+    assert np.array_equal(stored(table), packed(present, values))
+    otab = ora.table(to_oracle_cfg(cfg))
+    otab.upload_store(table.download_store())
+    assert otab.check_admissibility() == 0
+    q = np.concatenate([present, absent])
+    want, hits, probes = otab.find_bulk(q)
+    got, stats = table.find(dev(q), want_stats=True)
+    assert hits == n and np.array_equal(host(got), want) and stats.probes == probes
+    # insert probes of the whole build = what the outcome reports; for bp2ht exactly 2 per pair (table.cpp:109-130)
+    if kind == "bp2ht":
+        assert o.probes == 2 * n
+    # a second chunked build into the now non-empty table, and an empty one
+    if lf <= 0.85:
+        more, mv = absent[:2000], random_values(2000, 3)
+        table.build_begin(2000)
+        table.build_feed(dev(more)[:1000], dev(mv)[:1000])
+        table.build_feed(dev(more)[1000:], dev(mv)[1000:])
+        o2 = table.build_end()
+        if o2.success:
+            assert np.array_equal(host(table.find(dev(more))), mv) and table.occupied_slots() == n + 2000
+    table.build_begin(0)
+    assert table.build_end().inserted == 0
+    table.close()
+
+
+def test_chunked_build_reports_overfull_table(bht):
+    """A chunked build that cannot place everything reports it like a bulk insert (the failed-build contract of
+    tests/test_gpu_edge.py): attempted = inserted + failed, every stored pair admissible, every stored pair found."""
+    n = 60_000
+    keys = unique_keys(n, 5)
+    vals = random_values(n, 5)
+    cfg = bht.make_config("bcht", 50_000, 1.0, 16, seed=9)  # 50 000 slots for 60 000 pairs
+    table = bht.HashTable(cfg, 0)
+    table.set_blocked_insert(3)
+    table.build_begin(n)
+    table.build_feed(dev(keys[:30_000]), dev(vals[:30_000]))
+    table.build_feed(dev(keys[30_000:]), dev(vals[30_000:]))
+    o = table.build_end()
+    assert not o.success and o.attempted == n and o.inserted + o.failed == n and o.failed >= n - cfg.capacity
+    assert table.occupied_slots() == o.inserted and table.count_inadmissible() == 0
+    got = host(table.find(dev(keys)))
+    assert int((got != EMPTY).sum()) == o.inserted and np.array_equal(got[got != EMPTY], vals[got != EMPTY])
+
+
+@pytest.mark.parametrize("mode", [0, 1, 3])
+def test_chain_cap_of_zero_fails_without_eviction(bht, ora, mode):
+    """max_chain = 0: the cap is tested BEFORE the exchange (table.cpp:67), so a pair whose bucket is full fails at once
+    and nothing is ever evicted — in every schedule (the blocked build, whose region pass evicts in shared memory,
+    must stand aside).  Compared with the oracle's sequential build of the same keys: same number of stored pairs is
+    not guaranteed under concurrency, but the invariants are: no victim is dropped (every stored pair sits in its H0
+    bucket), attempted = inserted + failed, and the call terminates."""
+    n = 120_000
+    keys = unique_keys(n, 31)
+    vals = random_values(n, 31)
+    cfg = bht.make_config("bcht", n, 0.97, 8, seed=21, max_chain=0)
+    assert cfg.max_chain == 0
+    table = bht.HashTable(cfg, 0)
+    table.set_blocked_insert(mode)
+    o = table.insert(dev(keys), dev(vals))
+    assert o.attempted == n and o.inserted + o.failed == n and o.failed > 0 and not o.success
+    assert table.occupied_slots() == o.inserted and table.count_inadmissible() == 0
+    store = table.download_store()
+    occ = store != np.uint64(0xFFFFFFFFFFFFFFFF)
+    skeys = (store[occ] & np.uint64(0xFFFFFFFF)).astype(np.uint32)
+    slot_bucket = (np.flatnonzero(occ) // cfg.bucket_size).astype(np.uint64)
+    a, b_, r = cfg.hashes[0]
+    h0 = np.array([bht.bucket_index(a, b_, r, int(k)) for k in skeys[:5000]], dtype=np.uint64)
+    assert np.array_equal(h0, slot_bucket[:5000])  # nothing was ever evicted to a later hash function
+    # Nothing moves once placed, so WHICH pairs are stored depends on arrival order but HOW MANY does not: every bucket
+    # keeps min(arrivals, b).  The oracle's sequential build of the same keys stores the same number, and every
+    # insertion — placed or failed — costs max_chain + 1 = 1 probe.
+    otab = ora.table(to_oracle_cfg(cfg))
+    res = otab.insert_all(keys, vals)
+    assert res["inserted"] == o.inserted and res["probes"] == n == o.probes
+    table.close()
+
+
+def test_host_buffer_build_takes_the_blocked_pipeline_and_returns_early(bht, ora):
+    """bht_insert(BHT_MEM_HOST) of a batch that qualifies for the shared-memory-blocked build: chunks go through the
+    first partition pass as they land, the call returns when the host arrays have been read, and everything done with
+    the table afterwards (host find, device find on the same stream, the outcome) is ordered after the build."""
+    n = 6_000_000
+    cfg = bht.make_config("bcht", n, 0.9, 16, seed=bht.mix_seed(3, 1))
+    keys_d, vals_d = bht.generate_unique_keys(11, 0, n, device=0)
+    h_keys = keys_d.cpu().pin_memory()
+    h_vals = vals_d.cpu().pin_memory()
+    table = bht.HashTable(cfg, 0)
+    table.set_blocked_insert(3)
+    for values in (h_vals, None):
+        table.clear()
+        launches0 = bht.kernel_launch_count()
+        assert table.insert(h_keys, values, want_result=False) is None
+        out = table.find(h_keys)  # host in / host out, enqueued while the build may still be running
+        o = table.last_insert_result()
+        assert o.success and o.inserted == n
+        want = h_vals if values is not None else bht.values_for_keys(keys_d.view(torch.int32)).cpu()
+        assert torch.equal(out.view(torch.int32), want.view(torch.int32))
+        assert table.occupied_slots() == n and table.count_inadmissible() == 0
+        assert bht.kernel_launch_count() - launches0 < 60  # one K8g per chunk + K10 + K11 + K4, not a probe kernel per chunk
+    # the same pairs through the per-chunk general kernel (mode 0) give the same multiset
+    t0 = bht.HashTable(cfg, 0)
+    t0.set_blocked_insert(0)
+    assert t0.insert(h_keys, None).success
+    assert np.array_equal(stored(t0), stored(table))
+    t0.close()
+    table.close()
+
+
+def test_deferred_fill_is_ordered_across_streams(bht):
+    """bht_clear defers the fill of a large bcht table; the first user pays it on ITS stream.  A second user on another
+    stream must not read the store before that fill has run (it waits on the fill's event)."""
+    n = 3_000_000
+    cfg = bht.make_config("bcht", n, 0.9, 16, seed=4)
+    keys_d, vals_d = bht.generate_unique_keys(5, 0, n, device=0)
+    table = bht.HashTable(cfg, 0)
+    table.set_blocked_insert(3)
+    assert table.insert(keys_d.view(torch.int32), vals_d.view(torch.int32)).success
+    sa, sb = torch.cuda.Stream(), torch.cuda.Stream()
+    for _ in range(5):
+        table.clear()  # deferred: the store still holds the previous build
+        torch.cuda.synchronize()
+        with torch.cuda.stream(sa):
+            # a long-running kernel first, so that the fill this find triggers is still pending when B starts
+            junk = torch.empty(256 << 20, dtype=torch.uint8, device="cuda").fill_(1)
+            a = table.find(keys_d.view(torch.int32), stream=sa)
+        with torch.cuda.stream(sb):
+            b = table.find(keys_d.view(torch.int32), stream=sb)
+        torch.cuda.synchronize()
+        assert int((a.view(torch.int32) != -1).sum()) == 0
+        assert int((b.view(torch.int32) != -1).sum()) == 0, "a find on another stream read the store before the deferred fill"
+        del junk
+    table.close()

@@ -161,6 +161,7 @@ def test_build_parity_routed(bht, ora, monkeypatch, kind, b, lf, t, mode):
     present, absent = keys[:n], keys[n:]
     values = random_values(n, 11 * b)
     monkeypatch.setenv("BHT_REGION_MB", "1")
+    bht.reload_tuning()  # the knobs are read once per process
     for attempt in range(20):
         cfg = bht.make_config(kind, n, lf, b, threshold=t, seed=bht.mix_seed(13, 0x100 + attempt))
         table = bht.HashTable(cfg, 0)

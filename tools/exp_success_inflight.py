@@ -11,7 +11,7 @@ trials = int(sys.argv[3]) if len(sys.argv) > 3 else 60
 keys = workload.generate_keys(bht.mix_seed(1, 0x6B657973), n, device=0).keys.view(torch.int32)
 vals = bht.values_for_keys(keys)
 for ctas in ("0", "148", "16", "1"):
-    os.environ["BHT_INSERT_GRID"] = ctas
+    os.environ["BHT_INSERT_GRID"] = ctas; bht.reload_tuning()
     ok, dropped = 0, 0
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ms = 0.0

@@ -18,12 +18,12 @@ for tail_frac, grid in ((0.0, "0"), (0.005, "1"), (0.02, "1"), (0.02, "16"), (0.
         cfg = bht.make_config("bcht", n, lf, 16, seed=bht.mix_seed(1234, t))
         table = bht.HashTable(cfg, 0)
         table.set_blocked_insert(0)
-        os.environ["BHT_INSERT_GRID"] = "0"
+        os.environ["BHT_INSERT_GRID"] = "0"; bht.reload_tuning()
         ev0.record()
         o1 = table.insert(keys[:k1], vals[:k1])
         failed = o1.failed
         if k1 < n:
-            os.environ["BHT_INSERT_GRID"] = grid
+            os.environ["BHT_INSERT_GRID"] = grid; bht.reload_tuning()
             failed += table.insert(keys[k1:], vals[k1:]).failed
         ev1.record(); ev1.synchronize()
         ms += ev0.elapsed_time(ev1)

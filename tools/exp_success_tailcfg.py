@@ -15,9 +15,9 @@ CONFIGS = [("0", "", "")] + [("1", lf_, d_) for lf_ in ("0.96", "0.975", "0.985"
 if len(sys.argv) > 4:
     CONFIGS = [tuple(c.split(":")) for c in sys.argv[4:]]
 for thr, tail_lf, div in CONFIGS:
-    os.environ["BHT_TAIL_THROTTLE"] = thr
+    os.environ["BHT_TAIL_THROTTLE"] = thr; bht.reload_tuning()
     if tail_lf:
-        os.environ["BHT_TAIL_LF"], os.environ["BHT_TAIL_DIV"] = tail_lf, div
+        os.environ["BHT_TAIL_LF"], os.environ["BHT_TAIL_DIV"] = tail_lf, div; bht.reload_tuning()
     ok, dropped, ms = 0, 0, 0.0
     for t in range(trials):
         cfg = bht.make_config("bcht", n, lf, 16, seed=bht.mix_seed(1234, t))
