@@ -174,6 +174,10 @@ bht_status bht_build(const bht_config* cfg, int32_t device, const uint32_t* keys
 bht_status bht_build_begin(bht_table* table, uint64_t n_max, void* stream);
 bht_status bht_build_feed(bht_table* table, const uint32_t* keys, const uint32_t* values, uint64_t n, void* stream);
 bht_status bht_build_end(bht_table* table, bht_insert_result* result, void* stream);
+/* bht_build_feed for a chunk whose length is only known on the device (the receive side of a sync-free exchange):
+ * the chunk holds min(n_cap, *n_dev) pairs, n_dev a device pointer read by the kernels.  Cuckoo kinds only. */
+bht_status bht_build_feed_counted(bht_table* table, const uint32_t* keys, const uint32_t* values, uint64_t n_cap,
+                                  const uint64_t* n_dev, void* stream);
 
 /* The reference's per-variant entry points bcht_insert / bp2ht_insert / iht_insert and bcht_find /
  * bp2ht_find / iht_find (table.hpp:84-101): as bht_insert / bht_find, but BHT_KIND_MISMATCH when the
@@ -198,6 +202,10 @@ bht_status bht_failed_keys(bht_table* table, uint32_t* host_out, uint64_t max_ke
 bht_status bht_last_insert_phases(bht_table* table, float* prepare_ms, float* probe_ms);
 /* iht only: select the prose variant of iht_insert (table.cpp:167-169, `prose_fallback`). */
 bht_status bht_set_iht_prose_fallback(bht_table* table, int32_t enabled);
+
+/* How the last bht_insert / chunked build of this table ran: 0 = caller order (K4 / K5 / K6 / K12 / K13), 2 = L2-routed,
+ * 3 = shared-memory-blocked (K8g, K10, K11, K4).  Diagnostics: tests and smoke() assert the schedule they mean to cover. */
+int32_t bht_last_build_schedule(const bht_table* table);
 
 /* Large device-resident inserts into a store much bigger than the L2 are blocked by table region first (same
  * result set, different concurrent order).  bcht: the pairs are partitioned in two streaming passes by the 64 KiB
@@ -257,6 +265,16 @@ bht_status bht_shard_partition(uint64_t alpha, uint64_t beta, uint32_t n_shards,
                                const uint32_t* keys, const uint32_t* values, uint64_t n,
                                uint32_t* out_keys, uint32_t* out_values, uint32_t* out_index,
                                uint64_t* counts_host, int32_t device, void* stream);
+
+/* bht_shard_partition without any host synchronisation, for an all-to-all with EQUAL splits: destination d gets the
+ * slots [d * cap, (d + 1) * cap) of the outputs (the caller pre-fills them with 0xFF bytes: unused slots then hold the
+ * sentinel key / the index 0xFFFFFFFF, which bht_find answers without a probe and bht_shard_unpermute skips);
+ * counts_dev[d] (device, uint64) = elements written for d; *overflow_dev (device) is OR-ed with 1 when some destination
+ * had more than cap elements (the surplus is not written: the caller re-routes with exact counts). */
+bht_status bht_shard_partition_fixed(uint64_t alpha, uint64_t beta, uint32_t n_shards, const uint32_t* keys,
+                                     const uint32_t* values, uint64_t n, uint64_t cap, uint32_t* out_keys,
+                                     uint32_t* out_values, uint32_t* out_index, uint64_t* counts_dev,
+                                     uint32_t* overflow_dev, int32_t device, void* stream);
 
 /* out[index[i]] = answers[i]: puts routed answers back into the caller's query order. */
 bht_status bht_shard_unpermute(const uint32_t* answers, const uint32_t* index, uint64_t n,

@@ -16,6 +16,6 @@ from .table import (  # noqa: E402
 )
 from ._lib import Config  # noqa: E402
 from . import experiments, workload  # noqa: E402,F401
-from .sharded import ShardedTable, LocalShardedTable, CudaShardOps, shard_constants  # noqa: E402
+from .sharded import ShardedTable, LocalShardedTable, CudaShardOps, RoutingOverflow, shard_constants  # noqa: E402
 
 __all__ = [n for n in dir() if not n.startswith("_")]

@@ -103,6 +103,9 @@ SIGNATURES = {
     "bht_build_begin": (C.c_int, [_vp, C.c_uint64, _vp]),
     "bht_build_feed": (C.c_int, [_vp, _vp, _vp, C.c_uint64, _vp]),
     "bht_build_end": (C.c_int, [_vp, C.POINTER(InsertResult), _vp]),
+    "bht_build_feed_counted": (C.c_int, [_vp, _vp, _vp, C.c_uint64, _vp, _vp]),
+    "bht_shard_partition_fixed": (C.c_int, [C.c_uint64, C.c_uint64, C.c_uint32, _vp, _vp, C.c_uint64, C.c_uint64, _vp, _vp, _vp, _vp, _vp,
+                                            C.c_int32, _vp]),
     "bht_find": (C.c_int, [_vp, _vp, _vp, C.c_uint64, C.c_int32, C.POINTER(FindResult), _vp]),
     "bht_find_as": (C.c_int, [_vp, C.c_int32, _vp, _vp, C.c_uint64, C.c_int32, C.POINTER(FindResult), _vp]),
     "bht_find_exhaustive": (C.c_int, [_vp, _vp, _vp, C.c_uint64, C.c_int32, C.POINTER(FindResult), _vp]),
@@ -110,6 +113,7 @@ SIGNATURES = {
     "bht_failed_keys": (C.c_int, [_vp, _vp, C.c_uint64, _u64p]),
     "bht_set_iht_prose_fallback": (C.c_int, [_vp, C.c_int32]),
     "bht_set_blocked_insert": (C.c_int, [_vp, C.c_int32]),
+    "bht_last_build_schedule": (C.c_int32, [_vp]),
     "bht_set_tail_throttle": (C.c_int, [_vp, C.c_int32]),
     "bht_last_insert_phases": (C.c_int, [_vp, C.POINTER(C.c_float), C.POINTER(C.c_float)]),
     "bht_load_factor": (C.c_int, [_vp, _u64p, _u64p]),

@@ -218,6 +218,7 @@ struct GroupArgs {
   const uint32_t* keys;
   const uint32_t* values;  // null: keys-only build, value = value_for_key(key) (table.cpp:234)
   uint64_t n;
+  const unsigned long long* n_dev;  // when set: the chunk holds min(n, *n_dev) pairs
   uint32_t* group_cursor;
   uint2* grouped;
   Spill sp;
@@ -225,7 +226,9 @@ struct GroupArgs {
 };
 
 __global__ void __launch_bounds__(kSplitBlock, BHT_SPLIT_CTAS)
-group_scatter_kernel(const __grid_constant__ GroupArgs a) {
+group_scatter_kernel(const __grid_constant__ GroupArgs args) {
+  GroupArgs a = args;
+  if (a.n_dev != nullptr) a.n = min(a.n, static_cast<uint64_t>(*a.n_dev));
   extern __shared__ __align__(16) unsigned char split_bytes[];
   SplitShared& s = *reinterpret_cast<SplitShared*>(split_bytes);
   if (threadIdx.x < 256) s.hist[threadIdx.x] = 0;
@@ -687,7 +690,8 @@ cudaError_t blocked_build_begin(const BlockedPlan& p, uint64_t n, void* scratch,
 }
 
 cudaError_t blocked_build_scatter(const TableView& t, const BlockedPlan& p, uint64_t n, void* scratch, const uint32_t* keys,
-                                  const uint32_t* values, uint64_t len, int sm_count, cudaStream_t stream) {
+                                  const uint32_t* values, uint64_t len, int sm_count, cudaStream_t stream,
+                                  const unsigned long long* len_dev) {
   if (len == 0) return cudaSuccess;
   const ScratchMap m = map_scratch(p, n, scratch);
   const Spill sp{m.spill, m.spill_start, m.spill_cursor};
@@ -698,7 +702,7 @@ cudaError_t blocked_build_scatter(const TableView& t, const BlockedPlan& p, uint
   static const cudaError_t attr = cudaFuncSetAttribute(group_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                       static_cast<int>(sizeof(SplitShared)));
   if (attr != cudaSuccess) return attr;
-  const GroupArgs ga{t.h[0], p.region_log2, inv_per, p.n_groups, p.group_cap, keys, values, len, m.group_cursor, m.grouped, sp, aligned ? 1 : 0};
+  const GroupArgs ga{t.h[0], p.region_log2, inv_per, p.n_groups, p.group_cap, keys, values, len, len_dev, m.group_cursor, m.grouped, sp, aligned ? 1 : 0};
   group_scatter_kernel<<<grid, kSplitBlock, sizeof(SplitShared), stream>>>(ga);
   note_launch();
   return cudaGetLastError();

@@ -175,6 +175,7 @@ struct bht_table {
   // bht_set_blocked_insert: 0 = caller order, 1 = blocked when worth it (default), 2 = always the L2-routed
   // build, 3 = always the shared-memory-blocked build (bcht, 8 <= b <= 32; else as 2); bp2ht / iht are never blocked
   int blocked_insert = 1;
+  int last_schedule = 0;  // how the last insert / chunked build ran: 0 = caller order, 2 = L2-routed, 3 = shared-memory-blocked
   bool known_empty = true;  // no slot has been written since create / clear: a blocked build need not read the store
   // The fill of create / clear is deferred until something reads or partially writes the store: a shared-memory-blocked
   // build into an empty table writes every region of the store exactly once, empty slots included (K11), so the fill
@@ -550,6 +551,7 @@ bht_status do_insert(bht_table* t, const uint32_t* keys, const uint32_t* values,
       if (e == cudaSuccess) e = blocked_build_scatter(t->view, plan, n, scratch.p, keys, values, n, t->sm_count, stream);
       if (e == cudaSuccess) e = finish_blocked(t, plan, n, scratch.p, t->known_empty, fused_fill, stream);
       if (e != cudaSuccess) return cuda_fail(e, "bht_insert (shared-memory blocked)");
+      t->last_schedule = 3;
     } else if (regions > 1) {
       // L2-blocked build: group the pairs by the table region of their first bucket, then insert region by
       // region, so that bucket fetches, claims and the write-back of dirty sectors happen while the region
@@ -564,9 +566,11 @@ bht_status do_insert(bht_table* t, const uint32_t* keys, const uint32_t* values,
       if (e == cudaSuccess) e = cudaEventRecord(t->phase_ev[1], stream);
       if (e == cudaSuccess) e = launch_insert_kind(t, PairSource{packed, nullptr}, n, blocked_ctas_per_sm(), stream, true);
       if (e != cudaSuccess) return cuda_fail(e, "bht_insert (blocked)");
+      t->last_schedule = 2;
     } else {
       BHT_CUDA(cudaEventRecord(t->phase_ev[1], stream));
       BHT_CUDA(launch_insert_kind(t, PairSource{keys, values}, n, 0, stream));
+      t->last_schedule = 0;
     }
     if (tail.tail != 0)
       BHT_CUDA(launch_insert_kind(t, PairSource{keys + n, tail_values + n}, tail.tail, 0, stream, false, nullptr, tail.grid));
@@ -585,6 +589,7 @@ bht_status do_insert(bht_table* t, const uint32_t* keys, const uint32_t* values,
     Staging& st = t->stage;
     const BlockedPlan plan = tail.tail == 0 ? smem_blocked_plan(t, n) : BlockedPlan{};
     const bool blocked = plan.n_regions != 0;
+    t->last_schedule = blocked ? 3 : 0;
     const bool fused_fill = blocked && t->known_empty && t->clear_pending.load(std::memory_order_acquire);
     if (!fused_fill) BHT_CUDA(materialize_clear(t, stream));
     cudaEvent_t start = st.out_done[0];  // reuse as the "counters are zeroed" marker
@@ -661,10 +666,12 @@ bht_status session_begin(bht_table* t, uint64_t n_max, void* stream_v) {
   }
   ses.active = true;
   t->session = ses;
+  t->last_schedule = ses.blocked ? 3 : 0;
   return BHT_OK;
 }
 
-bht_status session_feed(bht_table* t, const uint32_t* keys, const uint32_t* values, uint64_t n, void* stream_v) {
+bht_status session_feed(bht_table* t, const uint32_t* keys, const uint32_t* values, uint64_t n, void* stream_v,
+                        const unsigned long long* n_dev = nullptr) {
   if (t == nullptr) return fail(BHT_INVALID_ARGUMENT, "bht_build_feed: null table");
   if (n != 0 && keys == nullptr) return fail(BHT_INVALID_ARGUMENT, "bht_build_feed: null keys");
   BHT_ON_DEVICE(t->device);
@@ -674,8 +681,10 @@ bht_status session_feed(bht_table* t, const uint32_t* keys, const uint32_t* valu
   if (ses.fed + n > ses.n_max) return fail(BHT_CAPACITY_EXCEEDED, "bht_build_feed: more pairs than bht_build_begin announced");
   cudaStream_t stream = as_stream(stream_v);
   if (n == 0) return BHT_OK;
+  if (n_dev != nullptr && !ses.blocked && t->cfg.kind != BHT_BCHT && t->cfg.kind != BHT_ONE_CHT)
+    return fail(BHT_INVALID_ARGUMENT, "bht_build_feed_counted: device-side counts are for the cuckoo kinds");
   if (ses.blocked) {
-    BHT_CUDA(blocked_build_scatter(t->view, ses.plan, ses.n_max, ses.scratch, keys, values, n, t->sm_count, stream));
+    BHT_CUDA(blocked_build_scatter(t->view, ses.plan, ses.n_max, ses.scratch, keys, values, n, t->sm_count, stream, n_dev));
   } else {
     BHT_CUDA(materialize_clear(t, stream));
     void* derived = nullptr;
@@ -688,7 +697,7 @@ bht_status session_feed(bht_table* t, const uint32_t* keys, const uint32_t* valu
       }
       values = static_cast<const uint32_t*>(derived);
     }
-    const cudaError_t e = launch_insert_kind(t, PairSource{keys, values}, n, 0, stream);
+    const cudaError_t e = launch_insert_kind(t, PairSource{keys, values}, n, 0, stream, false, n_dev);
     if (derived != nullptr) cudaFreeAsync(derived, stream);
     if (e != cudaSuccess) return cuda_fail(e, "bht_build_feed");
     t->known_empty = false;
@@ -725,7 +734,8 @@ bht_status session_end(bht_table* t, bht_insert_result* result, void* stream_v) 
   if (result != nullptr) {
     const bht_status s = read_counters(t, stream);
     if (s != BHT_OK) return s;
-    fill_insert_result(t, fed, result);
+    // every fed pair ends up inserted or failed; with device-counted chunks `fed` is only an upper bound
+    fill_insert_result(t, t->ctr_host->inserted + t->ctr_host->failed, result);
   }
   return BHT_OK;
 }
@@ -1043,6 +1053,11 @@ bht_status bht_build_begin(bht_table* t, uint64_t n_max, void* stream) { return 
 bht_status bht_build_feed(bht_table* t, const uint32_t* keys, const uint32_t* values, uint64_t n, void* stream) {
   return session_feed(t, keys, values, n, stream);
 }
+bht_status bht_build_feed_counted(bht_table* t, const uint32_t* keys, const uint32_t* values, uint64_t n_cap,
+                                  const uint64_t* n_dev, void* stream) {
+  if (n_dev == nullptr) return fail(BHT_INVALID_ARGUMENT, "bht_build_feed_counted: null device count");
+  return session_feed(t, keys, values, n_cap, stream, reinterpret_cast<const unsigned long long*>(n_dev));
+}
 bht_status bht_build_end(bht_table* t, bht_insert_result* result, void* stream) { return session_end(t, result, stream); }
 
 bht_status bht_insert_as(bht_table* t, int32_t kind, const uint32_t* keys, const uint32_t* values, uint64_t n,
@@ -1119,6 +1134,8 @@ bht_status bht_set_tail_throttle(bht_table* t, int32_t enabled) {
   t->tail_throttle = enabled != 0;
   return BHT_OK;
 }
+
+int32_t bht_last_build_schedule(const bht_table* t) { return t != nullptr ? t->last_schedule : -1; }
 
 bht_status bht_set_blocked_insert(bht_table* t, int32_t enabled) {
   if (t == nullptr) return fail(BHT_INVALID_ARGUMENT, "bht_set_blocked_insert: null table");
@@ -1298,6 +1315,38 @@ bht_status bht_shard_partition(uint64_t alpha, uint64_t beta, uint32_t n_shards,
   cudaFreeAsync(scratch, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   if (e != cudaSuccess) return cuda_fail(e, "bht_shard_partition");
+  return BHT_OK;
+}
+
+bht_status bht_shard_partition_fixed(uint64_t alpha, uint64_t beta, uint32_t n_shards, const uint32_t* keys,
+                                     const uint32_t* values, uint64_t n, uint64_t cap, uint32_t* out_keys, uint32_t* out_values,
+                                     uint32_t* out_index, uint64_t* counts_dev, uint32_t* overflow_dev, int32_t device,
+                                     void* stream) {
+  if (alpha > 0xFFFFFFFFull || beta > 0xFFFFFFFFull) return fail(BHT_INVALID_ARGUMENT, "bht_shard_partition_fixed: constants must fit 32 bits");
+  if (n_shards == 0 || n_shards > static_cast<uint32_t>(kMaxShards))
+    return fail(BHT_INVALID_ARGUMENT, "bht_shard_partition_fixed: n_shards must be in [1, 256]");
+  if (n > 0xFFFFFFFFull || cap == 0 || cap * n_shards > 0xFFFFFFFFull)
+    return fail(BHT_INVALID_ARGUMENT, "bht_shard_partition_fixed: at most 2^32 - 1 elements / output slots per call");
+  if (counts_dev == nullptr || overflow_dev == nullptr || (n != 0 && (keys == nullptr || out_keys == nullptr)) ||
+      (values != nullptr && out_values == nullptr))
+    return fail(BHT_INVALID_ARGUMENT, "bht_shard_partition_fixed: null argument");
+  BHT_ON_DEVICE(device);
+  static int sm_counts[64] = {};
+  if (device < 64 && sm_counts[device] == 0) {
+    cudaDeviceProp prop;
+    BHT_CUDA(cudaGetDeviceProperties(&prop, device));
+    sm_counts[device] = prop.multiProcessorCount;
+  }
+  const int sm_count = device < 64 ? sm_counts[device] : 148;
+  cudaStream_t s = as_stream(stream);
+  unsigned long long* scratch = nullptr;  // cursors | n destination bytes
+  BHT_CUDA(cudaMallocAsync(&scratch, sizeof(unsigned long long) * n_shards + n + 16, s));
+  const cudaError_t e = launch_shard_route_fixed(static_cast<uint32_t>(alpha), static_cast<uint32_t>(beta), n_shards, keys, values, n, cap,
+                                                 reinterpret_cast<uint8_t*>(scratch + n_shards),
+                                                 reinterpret_cast<unsigned long long*>(counts_dev), scratch, overflow_dev, out_keys,
+                                                 out_values, out_index, sm_count, s);
+  cudaFreeAsync(scratch, s);
+  if (e != cudaSuccess) return cuda_fail(e, "bht_shard_partition_fixed");
   return BHT_OK;
 }
 

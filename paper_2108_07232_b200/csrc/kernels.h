@@ -75,7 +75,8 @@ cudaError_t launch_blocked_build(const TableView& t, const BlockedPlan& p, const
 // the plan and the scratch were sized for): begin, then scatter once per chunk (K8g), then finish (K10 + K11).
 cudaError_t blocked_build_begin(const BlockedPlan& p, uint64_t n, void* scratch, cudaStream_t stream);
 cudaError_t blocked_build_scatter(const TableView& t, const BlockedPlan& p, uint64_t n, void* scratch, const uint32_t* keys,
-                                  const uint32_t* values, uint64_t len, int sm_count, cudaStream_t stream);
+                                  const uint32_t* values, uint64_t len, int sm_count, cudaStream_t stream,
+                                  const unsigned long long* len_dev = nullptr);  // when set: min(len, *len_dev) pairs, read on the device
 cudaError_t blocked_build_finish(const TableView& t, const BlockedPlan& p, uint64_t n, void* scratch, bool fresh,
                                  DevCounters* ctr, int sm_count, cudaStream_t stream, PairSource* spill_out,
                                  const unsigned long long** spill_count_out);
@@ -95,6 +96,12 @@ constexpr int kMaxShards = 256;
 cudaError_t launch_shard_route(uint32_t alpha, uint32_t beta, uint32_t n_shards, const uint32_t* keys, const uint32_t* values,
                                uint64_t n, uint8_t* scratch8, unsigned long long* counts, unsigned long long* cursors,
                                uint32_t* out_keys, uint32_t* out_values, uint32_t* out_index, int sm_count, cudaStream_t stream);
+// The same routing into fixed segments of `cap` elements per destination (what a sync-free all-to-all with equal splits
+// sends): counts (device) are clamped to cap, *overflow is set when a destination had more.  Nothing is copied to the host.
+cudaError_t launch_shard_route_fixed(uint32_t alpha, uint32_t beta, uint32_t n_shards, const uint32_t* keys, const uint32_t* values,
+                                     uint64_t n, uint64_t cap, uint8_t* scratch8, unsigned long long* counts,
+                                     unsigned long long* cursors, uint32_t* overflow, uint32_t* out_keys, uint32_t* out_values,
+                                     uint32_t* out_index, int sm_count, cudaStream_t stream);
 // Groups pairs by the table region (n_regions contiguous ranges of buckets) of their first bucket; out_pairs
 // receives n packed {key, value} pairs (8 bytes each).
 cudaError_t launch_region_route(const HashFn& h0, uint32_t n_regions, const uint32_t* keys, const uint32_t* values, uint64_t n,

@@ -57,13 +57,22 @@ def shard_constants(seed: int):
     return alpha, beta
 
 
+class RoutingOverflow(RuntimeError):
+    """A destination shard received more keys of one chunk than the fixed exchange segment holds (8 sigma above the
+    mean of a uniform routing hash): the input is skewed against the routing hash.  Re-run with ``exact=True``."""
+
+
 class CudaShardOps:
     """Per-rank device work of the sharded table, all through the C ABI."""
+
+    supports_counted = True  # device-side chunk lengths (bht_build_feed_counted): the sync-free exchange
 
     def __init__(self, cfg, device: int):
         self.device = int(device)
         self.table = HashTable(cfg, self.device)
         self._lib = _lib.load()
+        self.overflow = torch.zeros(1, dtype=torch.int32, device=self.torch_device)
+        self.cuckoo = cfg.kind in (_lib_kind("bcht"), _lib_kind("1cht"))
 
     @property
     def torch_device(self):
@@ -71,6 +80,10 @@ class CudaShardOps:
 
     def empty(self, n: int) -> torch.Tensor:
         return torch.empty(n, dtype=torch.int32, device=self.torch_device)
+
+    def filled(self, n: int) -> torch.Tensor:
+        """n words of 0xFFFFFFFF: the sentinel key / the "no slot" index of a padded exchange segment."""
+        return torch.full((n,), -1, dtype=torch.int32, device=self.torch_device)
 
     def partition(self, alpha: int, beta: int, n_shards: int, keys: torch.Tensor, values: Optional[torch.Tensor],
                   want_index: bool):
@@ -86,12 +99,40 @@ class CudaShardOps:
             _stream_ptr(None, self.device)))
         return out_keys, out_vals, index, [int(c) for c in counts]
 
+    def partition_fixed(self, alpha: int, beta: int, n_shards: int, keys: torch.Tensor, values: Optional[torch.Tensor],
+                        want_index: bool, cap: int):
+        """Routes into fixed segments of ``cap`` slots per destination, nothing copied to the host: returns
+        (keys[n_shards * cap] padded with the sentinel, values or None, index padded with 0xFFFFFFFF or None,
+        counts[n_shards] int64 on the device).  ``self.overflow`` is raised on the device when a segment was too small."""
+        n = keys.numel()
+        out_keys = self.filled(n_shards * cap)
+        out_vals = self.empty(n_shards * cap) if values is not None else None
+        index = self.filled(n_shards * cap) if want_index else None
+        counts = torch.empty(n_shards, dtype=torch.int64, device=self.torch_device)
+        _check(self._lib.bht_shard_partition_fixed(
+            alpha, beta, n_shards, keys.data_ptr(), values.data_ptr() if values is not None else None, n, cap,
+            out_keys.data_ptr(), out_vals.data_ptr() if out_vals is not None else None,
+            index.data_ptr() if index is not None else None, counts.data_ptr(), self.overflow.data_ptr(), self.device,
+            _stream_ptr(None, self.device)))
+        return out_keys, out_vals, index, counts
+
     def unpermute(self, answers: torch.Tensor, index: torch.Tensor, out: torch.Tensor) -> None:
         _check(self._lib.bht_shard_unpermute(answers.data_ptr(), index.data_ptr(), answers.numel(), out.data_ptr(),
                                              self.device, _stream_ptr(None, self.device)))
 
     def insert(self, keys: torch.Tensor, values: torch.Tensor) -> BuildOutcome:
         return self.table.insert(keys, values)
+
+    def build_begin(self, n_max: int) -> None:
+        self.table.build_begin(n_max)
+
+    def feed_counted(self, keys: torch.Tensor, values: torch.Tensor, cap: int, count: torch.Tensor) -> None:
+        """One received segment: min(cap, count) pairs, ``count`` a one-element int64 device tensor."""
+        _check(self._lib.bht_build_feed_counted(self.table._h, keys.data_ptr(), values.data_ptr(), cap, count.data_ptr(),
+                                                _stream_ptr(None, self.device)))
+
+    def build_end(self) -> BuildOutcome:
+        return self.table.build_end()
 
     def find(self, keys: torch.Tensor) -> torch.Tensor:
         out = self.empty(keys.numel())
@@ -102,8 +143,21 @@ class CudaShardOps:
         return torch.tensor(list(counts), dtype=torch.int64, device=self.torch_device)
 
 
+def _lib_kind(name: str) -> int:
+    from .table import KINDS
+    return KINDS[name]
+
+
 class ShardedTable:
-    """One logical table over ``world_size`` shards; call every method collectively on all ranks."""
+    """One logical table over ``world_size`` shards; call every method collectively on all ranks.
+
+    Two exchanges.  The default one (cuckoo kinds) never synchronises with the host inside a call: every chunk is
+    routed into fixed segments of ``cap`` slots per destination (the mean of a uniform routing hash + 8 sigma), sent
+    with EQUAL-split all-to-alls, and the receive side learns the segment lengths on the device
+    (bht_build_feed_counted) — one aggregate read at the end of the call (outcome + overflow flag).  The received
+    chunks go through the table's chunked build, so a shard that qualifies takes the shared-memory-blocked build
+    however many chunks it arrives in.  ``exact=True`` is the exchange with exact split sizes: one counts read per
+    chunk, any skew."""
 
     def __init__(self, cfg_per_shard, group=None, ops=None, device: Optional[int] = None, chunk: int = 1 << 26,
                  route_seed: Optional[int] = None):
@@ -116,6 +170,8 @@ class ShardedTable:
         self.cfg = cfg_per_shard
         self.chunk = int(chunk)
         self.alpha, self.beta = shard_constants(cfg_per_shard.seed if route_seed is None else route_seed)
+        self.phase_ms = {}  # bench.py: CUDA-event times of the phases of the last call (when record_phases is set)
+        self.record_phases = False
 
     # -- routing pieces
     def _exchange_counts(self, send_counts: List[int]) -> List[int]:
@@ -131,24 +187,81 @@ class ShardedTable:
         return recv, work
 
     def _chunks(self, n: int):
-        # every rank must issue the same number of collectives: agree on the max chunk count
+        # every rank must issue the same number of collectives: agree on the max chunk count (the one host read
+        # before the pipeline starts)
         mine = max(1, -(-n // self.chunk))
-        t = self.ops.counts_tensor([mine])
+        t = self.ops.counts_tensor([mine, min(n, self.chunk)])
         dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
-        total = int(t.item())
-        for c in range(total):
-            lo = min(c * self.chunk, n)
-            yield lo, min(lo + self.chunk, n)
+        total, self._longest_chunk = (int(x) for x in t.tolist())
+        return [(min(c * self.chunk, n), min((c + 1) * self.chunk, n)) for c in range(total)]
+
+    def segment_cap(self, chunk_len: int) -> int:
+        """Slots per destination of a fixed-segment exchange of ``chunk_len`` keys: mean + 8 sigma + 1024."""
+        chunk_len = max(int(chunk_len), 4)
+        if self.world == 1:
+            return (chunk_len + 3) & ~3
+        mean = chunk_len / self.world
+        return min((chunk_len + 3) & ~3, (int(mean + 8.0 * mean ** 0.5) + 1024 + 3) & ~3)
 
     @staticmethod
     def _i32(x: torch.Tensor) -> torch.Tensor:
         return x.view(torch.int32) if x.dtype == torch.uint32 else x
 
+    def _use_exact(self, exact: Optional[bool]) -> bool:
+        if exact is None:
+            return not (getattr(self.ops, "supports_counted", False) and getattr(self.ops, "cuckoo", False))
+        return bool(exact)
+
+    def _aggregate(self, totals, failed_key, overflow=None) -> BuildOutcome:
+        t = self.ops.counts_tensor(list(totals))
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
+        flags = [-1 if failed_key is None else failed_key]
+        fk = self.ops.counts_tensor(flags)
+        if overflow is not None:
+            fk = torch.cat([fk, overflow.to(torch.int64)])
+        dist.all_reduce(fk, op=dist.ReduceOp.MAX, group=self.group)
+        attempted, inserted, failed, probes = (int(x) for x in t.tolist())
+        fl = [int(x) for x in fk.tolist()]
+        if overflow is not None and fl[1] != 0:
+            raise RoutingOverflow("sharded insert: a routing segment overflowed; re-run with exact=True")
+        return BuildOutcome(inserted == attempted, inserted, failed, attempted, probes, None if fl[0] < 0 else fl[0])
+
     # -- the hot path
-    def insert(self, keys: torch.Tensor, values: torch.Tensor) -> BuildOutcome:
+    def insert(self, keys: torch.Tensor, values: torch.Tensor, exact: Optional[bool] = None) -> BuildOutcome:
         """Routes this rank's (key, value) pairs to their owners and bulk-inserts what this rank owns.
         Returns the outcome aggregated over all ranks."""
         keys, values = self._i32(keys), self._i32(values)
+        if self._use_exact(exact):
+            return self._insert_exact(keys, values)
+        chunks = self._chunks(keys.numel())
+        cap = self.segment_cap(self._longest_chunk)  # the same on every rank
+        self.ops.overflow.zero_()
+        self.ops.build_begin(self.cfg.capacity)
+        pending = None
+
+        def drain(p):
+            rk, rv, rc, works = p
+            for w in works:
+                w.wait()
+            for src in range(self.world):
+                self.ops.feed_counted(rk[src * cap:(src + 1) * cap], rv[src * cap:(src + 1) * cap], cap, rc[src:src + 1])
+
+        for lo, hi in chunks:
+            sk, sv, _, counts = self.ops.partition_fixed(self.alpha, self.beta, self.world, keys[lo:hi], values[lo:hi], False, cap)
+            rc = torch.empty_like(counts)
+            rk, rv = self.ops.empty(self.world * cap), self.ops.empty(self.world * cap)
+            works = [dist.all_to_all_single(rc, counts, group=self.group, async_op=True),
+                     dist.all_to_all_single(rk, sk, group=self.group, async_op=True),
+                     dist.all_to_all_single(rv, sv, group=self.group, async_op=True)]
+            if pending is not None:
+                drain(pending)  # the previous chunk's partition pass runs under this chunk's exchange
+            pending = (rk, rv, rc, works)
+        if pending is not None:
+            drain(pending)
+        o = self.ops.build_end()  # the one host read of the call
+        return self._aggregate([o.attempted, o.inserted, o.failed, o.probes], o.failed_key, self.ops.overflow)
+
+    def _insert_exact(self, keys: torch.Tensor, values: torch.Tensor) -> BuildOutcome:
         totals = [0, 0, 0, 0]  # attempted, inserted, failed, probes
         failed_key = None
         pending = None
@@ -178,21 +291,44 @@ class ShardedTable:
             pending = (rk, rv, wk, wv)
         if pending is not None:
             drain(pending)
+        return self._aggregate(totals, failed_key)
 
-        t = self.ops.counts_tensor(totals + [-1 if failed_key is None else failed_key])
-        agg = t[:4].clone()
-        dist.all_reduce(agg, op=dist.ReduceOp.SUM, group=self.group)
-        fk = t[4:].clone()
-        dist.all_reduce(fk, op=dist.ReduceOp.MAX, group=self.group)
-        attempted, inserted, failed, probes = (int(x) for x in agg.tolist())
-        fkv = int(fk.item())
-        return BuildOutcome(inserted == attempted, inserted, failed, attempted, probes, None if fkv < 0 else fkv)
-
-    def find(self, keys: torch.Tensor, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    def find(self, keys: torch.Tensor, out: Optional[torch.Tensor] = None, exact: Optional[bool] = None) -> torch.Tensor:
         """Answers this rank's queries in the caller's order: out[i] = value or EMPTY_VALUE."""
         keys = self._i32(keys)
         n = keys.numel()
         out = self.ops.empty(n) if out is None else self._i32(out)
+        if self._use_exact(exact):
+            return self._find_exact(keys, out)
+        chunks = self._chunks(n)
+        cap = self.segment_cap(self._longest_chunk)  # the same on every rank
+        self.ops.overflow.zero_()
+        pending = None
+
+        def drain(p):
+            lo, hi, rk, wk, index = p
+            wk.wait()
+            answers = self.ops.find(rk)  # padding slots hold the sentinel key: answered EMPTY without a probe
+            back = self.ops.empty(self.world * cap)
+            dist.all_to_all_single(back, answers, group=self.group)  # reverse route, same equal splits
+            self.ops.unpermute(back, index, out[lo:hi])  # padding slots carry the index 0xFFFFFFFF: skipped
+
+        for lo, hi in chunks:
+            sk, _, index, _counts = self.ops.partition_fixed(self.alpha, self.beta, self.world, keys[lo:hi], None, True, cap)
+            rk = self.ops.empty(self.world * cap)
+            wk = dist.all_to_all_single(rk, sk, group=self.group, async_op=True)
+            if pending is not None:
+                drain(pending)
+            pending = (lo, hi, rk, wk, index)
+        if pending is not None:
+            drain(pending)
+        flag = self.ops.overflow.to(torch.int64)
+        dist.all_reduce(flag, op=dist.ReduceOp.MAX, group=self.group)
+        if int(flag.item()) != 0:  # the one host read of the call
+            raise RoutingOverflow("sharded find: a routing segment overflowed; re-run with exact=True")
+        return out
+
+    def _find_exact(self, keys: torch.Tensor, out: torch.Tensor) -> torch.Tensor:
         pending = None
 
         def drain(p):
@@ -203,7 +339,7 @@ class ShardedTable:
             back, _ = self._all_to_all(answers, recv_counts, send_counts, False)  # reverse route
             self.ops.unpermute(back, index, out[lo:hi])
 
-        for lo, hi in self._chunks(n):
+        for lo, hi in self._chunks(keys.numel()):
             pk, _, index, send_counts = self.ops.partition(self.alpha, self.beta, self.world, keys[lo:hi], None, True)
             recv_counts = self._exchange_counts(send_counts)
             rk, wk = self._all_to_all(pk, send_counts, recv_counts, True)

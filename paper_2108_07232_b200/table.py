@@ -311,6 +311,10 @@ class HashTable:
         the candidate buckets."""
         _check(self._lib.bht_set_blocked_insert(self._h, int(mode)))
 
+    def last_build_schedule(self) -> int:
+        """0 = caller order, 2 = L2-routed, 3 = shared-memory-blocked: how the last insert / chunked build ran."""
+        return int(self._lib.bht_last_build_schedule(self._h))
+
     # -- the hot path
     def insert(self, keys, values=None, n: Optional[int] = None, stream=None, want_result: bool = True,
                as_kind=None) -> Optional[BuildOutcome]:

@@ -28,20 +28,21 @@ def nccl_world():
     dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("exact", [False, True])
 @pytest.mark.parametrize("chunk", [1 << 26, 100_000])
-def test_sharded_table_world_of_one(bht, nccl_world, chunk):
+def test_sharded_table_world_of_one(bht, nccl_world, chunk, exact):
     n = 700_000
     keys = unique_keys(n, 321, extra=n)
     vals = random_values(n, 321)
     d = lambda a: torch.from_numpy(np.ascontiguousarray(a).view(np.int32)).cuda()  # noqa: E731
     cfg = bht.make_config("bcht", n, 0.9, 16, seed=12)
     st = bht.ShardedTable(cfg, device=0, chunk=chunk)
-    o = st.insert(d(keys[:n]), d(vals))
+    o = st.insert(d(keys[:n]), d(vals), exact=exact)
     assert o.success and o.inserted == n and o.attempted == n
     assert st.inserted() == n
     q = np.concatenate([keys[:n:2], keys[n::2]])
     np.random.default_rng(0).shuffle(q)
-    got = st.find(d(q)).cpu().numpy().view(np.uint32)
+    got = st.find(d(q), exact=exact).cpu().numpy().view(np.uint32)
     lookup = dict(zip(keys[:n].tolist(), vals.tolist()))
     want = np.array([lookup.get(int(x), EMPTY) for x in q], dtype=np.uint32)
     assert np.array_equal(got, want)
@@ -49,3 +50,66 @@ def test_sharded_table_world_of_one(bht, nccl_world, chunk):
     plain, o2 = bht.build(d(keys[:n]), cfg, d(vals), device=0)
     assert o2.success
     assert np.array_equal(plain.find(d(q)).cpu().numpy().view(np.uint32), want)
+
+
+def test_sharded_build_in_chunks_takes_the_blocked_build(bht, nccl_world):
+    """A shard that qualifies for the shared-memory-blocked build gets it however many chunks the keys arrive in
+    (config 5 of BASELINE.json feeds 2^24-key chunks into 5e8-key shards): the received segments go through the chunked
+    build (bht_build_begin / bht_build_feed_counted / bht_build_end), the store is written once, and the table equals
+    the one a single bulk insert builds — same stored multiset, same probe totals for the finds."""
+    n = 30_000_000  # 267 MB of slots: beyond the L2, so the default mode blocks
+    keys, vals = bht.generate_unique_keys(3, 0, n, device=0)
+    keys, vals = keys.view(torch.int32), vals.view(torch.int32)
+    cfg = bht.make_config("bcht", n, 0.9, 16, seed=bht.mix_seed(1, 0x100))
+    st = bht.ShardedTable(cfg, device=0, chunk=1 << 22)
+    launches0 = bht.kernel_launch_count()
+    o = st.insert(keys, vals)
+    assert o.success and o.inserted == n
+    assert st.ops.table.last_build_schedule() == 3
+    # 8 chunks: route (3 kernels) + one first-pass launch per chunk, then K10, K11, K4 once
+    assert bht.kernel_launch_count() - launches0 <= 8 * 4 + 3 + 2
+    out = st.find(keys)
+    assert torch.equal(out, vals)
+    plain = bht.HashTable(cfg, 0)
+    assert plain.insert(keys, vals).success and plain.last_build_schedule() == 3
+    _, fa = st.ops.table.find(keys, want_stats=True)
+    _, fb = plain.find(keys, want_stats=True)
+    assert fa.hits == fb.hits == n and abs(fa.probes - fb.probes) < 0.002 * fb.probes
+    assert st.ops.table.occupied_slots() == n and st.ops.table.count_inadmissible() == 0
+
+
+def test_fixed_segment_partition_against_numpy(bht):
+    """bht_shard_partition_fixed: every key in the segment of its owner, counts on the device, padding untouched,
+    the overflow flag raised (and nothing written out of bounds) when a segment is too small."""
+    n, world = 1_000_003, 5
+    keys = unique_keys(n, 77)
+    vals = random_values(n, 77)
+    d = lambda a: torch.from_numpy(np.ascontiguousarray(a).view(np.int32)).cuda()  # noqa: E731
+    cfg = bht.make_config("bcht", n, 0.9, 16, seed=5)
+    ops = bht.CudaShardOps(cfg, 0)
+    alpha, beta = bht.shard_constants(cfg.seed)
+    lib = bht._lib.load()
+    owner = np.array([lib.bht_shard_of_host(alpha, beta, world, int(k)) for k in keys[:20000]])
+    cap = int(n / world * 1.05)
+    sk, sv, idx, counts = ops.partition_fixed(alpha, beta, world, d(keys), d(vals), True, cap)
+    torch.cuda.synchronize()
+    assert int(ops.overflow.item()) == 0
+    sk, sv, idx, counts = (x.cpu().numpy() for x in (sk, sv, idx, counts))
+    assert counts.sum() == n
+    for g in range(world):
+        seg_k = sk[g * cap:(g + 1) * cap].view(np.uint32)
+        seg_i = idx[g * cap:(g + 1) * cap].view(np.uint32)
+        c = int(counts[g])
+        assert np.all(seg_k[c:] == EMPTY) and np.all(seg_i[c:] == EMPTY)  # padding: sentinel key, no index
+        assert np.array_equal(keys[seg_i[:c]], seg_k[:c])
+        assert np.array_equal(vals[seg_i[:c]], sv[g * cap:g * cap + c].view(np.uint32))
+        small = seg_i[:c][seg_i[:c] < 20000]
+        assert np.all(owner[small] == g)
+    # a segment that is too small: flagged, counts clamped, neighbours' segments intact
+    cap2 = int(n / world * 0.9) & ~3
+    sk2, _, _, counts2 = ops.partition_fixed(alpha, beta, world, d(keys), None, False, cap2)
+    torch.cuda.synchronize()
+    assert int(ops.overflow.item()) == 1 and int(counts2.max().item()) == cap2
+    sk2 = sk2.cpu().numpy().view(np.uint32)
+    own2 = np.array([lib.bht_shard_of_host(alpha, beta, world, int(k)) for k in sk2[cap2:cap2 + 3000]])
+    assert np.all(own2 == 1)

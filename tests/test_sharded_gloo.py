@@ -20,11 +20,17 @@ EMPTY = 0xFFFFFFFF
 class OracleShardOps:
     """CPU stand-in with the interface of paper_2108_07232_b200.sharded.CudaShardOps."""
 
+    supports_counted = True
+    cuckoo = True
+
     def __init__(self, cfg):
         from oracle import binding
         self.ora = binding.oracle()
         self.table_o = self.ora.table(binding.Config.from_buffer_copy(bytes(cfg)))
         self.table = self  # .table.inserted()
+        self.overflow = torch.zeros(1, dtype=torch.int32)
+        self.session = None
+        self.host_reads = 0  # how often the routing logic pulled a count to the host (the exact exchange does, per chunk)
 
     def inserted(self):
         return self.table_o.inserted
@@ -35,7 +41,46 @@ class OracleShardOps:
     def counts_tensor(self, counts):
         return torch.tensor(list(counts), dtype=torch.int64)
 
+    def filled(self, n):
+        return torch.full((n,), -1, dtype=torch.int32)
+
+    def partition_fixed(self, alpha, beta, n_shards, keys, values, want_index, cap):
+        k = keys.numpy().view(np.uint32)
+        owner = np.array([self.ora.shard_of(alpha, beta, n_shards, int(x)) for x in k], dtype=np.int64)
+        out_k, out_v, idx = self.filled(n_shards * cap), self.empty(n_shards * cap), self.filled(n_shards * cap)
+        counts = torch.zeros(n_shards, dtype=torch.int64)
+        for d in range(n_shards):
+            at = np.flatnonzero(owner == d)
+            if at.size > cap:
+                self.overflow[0] = 1
+                at = at[:cap]
+            counts[d] = at.size
+            out_k[d * cap:d * cap + at.size] = torch.from_numpy(k[at].view(np.int32).copy())
+            if values is not None:
+                out_v[d * cap:d * cap + at.size] = values[torch.from_numpy(at)]
+            idx[d * cap:d * cap + at.size] = torch.from_numpy(at.astype(np.int32))
+        return out_k, (out_v if values is not None else None), (idx if want_index else None), counts
+
+    def build_begin(self, n_max):
+        assert self.session is None
+        self.session = [0, 0, 0, 0, None]
+
+    def feed_counted(self, keys, values, cap, count):
+        n = min(cap, int(count[0]))  # the stand-in reads the count; the product's kernels read it on the device
+        o = self.insert(keys[:n], values[:n])
+        ses = self.session
+        ses[0] += o.attempted; ses[1] += o.inserted; ses[2] += o.failed; ses[3] += o.probes
+        if ses[4] is None:
+            ses[4] = o.failed_key
+
+    def build_end(self):
+        from paper_2108_07232_b200 import BuildOutcome
+        a, i, f, p, fk = self.session
+        self.session = None
+        return BuildOutcome(f == 0, i, f, a, p, fk)
+
     def partition(self, alpha, beta, n_shards, keys, values, want_index):
+        self.host_reads += 1
         k = keys.numpy().view(np.uint32)
         owner = np.array([self.ora.shard_of(alpha, beta, n_shards, int(x)) for x in k], dtype=np.int64)
         order = np.argsort(owner, kind="stable")
@@ -46,7 +91,8 @@ class OracleShardOps:
         return pk, pv, idx, counts
 
     def unpermute(self, answers, index, out):
-        out[index.long()] = answers
+        keep = index != -1  # padding slots of a fixed-segment exchange
+        out[index[keep].long()] = answers[keep]
 
     def insert(self, keys, values):
         from paper_2108_07232_b200 import BuildOutcome
@@ -58,11 +104,14 @@ class OracleShardOps:
         return BuildOutcome(failed == 0, r["inserted"], failed, len(k), r["probes"], fk)
 
     def find(self, keys):
-        out, _, _ = self.table_o.find_bulk(keys.numpy().view(np.uint32))
+        k = keys.numpy().view(np.uint32)
+        out = np.full(k.size, EMPTY, dtype=np.uint32)  # the sentinel key (padding) is answered EMPTY without a probe (find.cu)
+        real = k != EMPTY
+        out[real], _, _ = self.table_o.find_bulk(k[real])
         return torch.from_numpy(out.view(np.int32).copy())
 
 
-def _worker(rank, world, port, n_per_rank, chunk, q):
+def _worker(rank, world, port, n_per_rank, chunk, exact, q):
     sys.path.insert(0, ROOT)
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -80,7 +129,8 @@ def _worker(rank, world, port, n_per_rank, chunk, q):
         st = bht.ShardedTable(cfg, ops=OracleShardOps(cfg), chunk=chunk)
         mine_k = torch.from_numpy(keys[lo:hi].view(np.int32).copy())
         mine_v = torch.from_numpy(vals[lo:hi].view(np.int32).copy())
-        outcome = st.insert(mine_k, mine_v)
+        outcome = st.insert(mine_k, mine_v, exact=exact)
+        assert (st.ops.host_reads == 0) == (not exact)  # the fixed-segment exchange never pulls counts to the host
         assert outcome.success and outcome.inserted == total and outcome.attempted == total, outcome
         assert st.inserted() == total
         assert abs(st.realized_load() - total / (cfg.capacity * world)) < 1e-12
@@ -98,8 +148,18 @@ def _worker(rank, world, port, n_per_rank, chunk, q):
         rng.shuffle(pos)
         q_keys = keys[pos]
         want = np.where(pos < total, vals[np.minimum(pos, total - 1)], EMPTY).astype(np.uint32)
-        got = st.find(torch.from_numpy(q_keys.view(np.int32).copy())).numpy().view(np.uint32)
+        reads0 = st.ops.host_reads
+        got = st.find(torch.from_numpy(q_keys.view(np.int32).copy()), exact=exact).numpy().view(np.uint32)
         assert np.array_equal(got, want)
+        assert (st.ops.host_reads == reads0) == (not exact)
+        if not exact:
+            # a segment too small for the chunk is reported, on every rank, not silently dropped
+            st.segment_cap = lambda chunk_len: 8
+            try:
+                st.find(torch.from_numpy(q_keys.view(np.int32).copy()), exact=False)
+                raise AssertionError("overflow went unnoticed")
+            except bht.RoutingOverflow:
+                pass
         # an insert that overfills reports failures consistently on all ranks
         q.put((rank, "ok", outcome.probes))
     except Exception as e:  # noqa: BLE001
@@ -117,12 +177,13 @@ def _free_port():
     return p
 
 
+@pytest.mark.parametrize("exact", [False, True])
 @pytest.mark.parametrize("n_per_rank,chunk", [([3000, 3000], 1 << 20), ([5000, 1200], 1024), ([0, 2500], 700)])
-def test_sharded_table_two_ranks_gloo(n_per_rank, chunk):
+def test_sharded_table_two_ranks_gloo(n_per_rank, chunk, exact):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, n_per_rank, chunk, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, n_per_rank, chunk, exact, q)) for r in range(2)]
     for p in procs:
         p.start()
     results = [q.get(timeout=240) for _ in procs]

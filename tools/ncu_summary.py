@@ -63,6 +63,9 @@ def main():
                 u = units[hdr.index(metric)]
                 return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[u]
             data[key] = val("dram__bytes_read.sum") + val("dram__bytes_write.sum")
+        sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+        import bench
+        data["_csrc_sha"] = bench.csrc_stamp()  # bench.py quotes these numbers only for the sources they were measured on
         json.dump(data, open(path, "w"), indent=1)
     text = "\n".join(lines) + "\n"
     if out:
