@@ -95,6 +95,22 @@ def make_workload(n: int, seed: int):
     return uniq[:n].copy(), uniq[n:2 * n].copy(), values
 
 
+class StdoutToStderr:
+    """Everything written to fd 1 inside the block goes to stderr: NCCL announces its version on stdout when the first
+    communicator comes up, and stdout carries exactly one JSON line."""
+
+    def __enter__(self):
+        sys.stdout.flush()
+        self.saved = os.dup(1)
+        os.dup2(2, 1)
+        return self
+
+    def __exit__(self, *exc):
+        sys.stdout.flush()
+        os.dup2(self.saved, 1)
+        os.close(self.saved)
+
+
 class ClockSampler:
     """SM clock and clock-event (throttle) reasons sampled DURING the timed region, every ~2 ms from a host thread
     through NVML (the timed region of the default run lasts tens of milliseconds, too short for `nvidia-smi -lms`);
@@ -227,7 +243,7 @@ def run_reference(args):
         "e2e": {"value": value, "unit": "MKeys/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "wall_s": time.time() - t0,
     }
-    print(json.dumps(line))
+    print(json.dumps(line), flush=True)
     return 0
 
 
@@ -268,7 +284,8 @@ def run_cuda(args):
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=device)
+        with StdoutToStderr():
+            dist.init_process_group("nccl", device_id=device)
     n = args.keys
     kw = {"threshold": THRESHOLD} if KIND == "iht" and THRESHOLD is not None else {}
     cfg_for = lambda attempt: bht.make_config(KIND, n, LF, B, seed=bht.mix_seed(SEED, 0x100 + attempt), **kw)  # noqa: E731
@@ -521,7 +538,7 @@ def run_cuda(args):
             "config": wl, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clocks, "detail": detail,
         }
-        print(json.dumps(line))
+        print(json.dumps(line), flush=True)
         return 0
 
     # ---- the sharded table (N > 1, or --sharded on one GPU): keys generated on the device, routing inside the timed region
@@ -531,7 +548,8 @@ def run_cuda(args):
         sk.bind(("127.0.0.1", 0))
         port = sk.getsockname()[1]
         sk.close()
-        dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1, device_id=device)
+        with StdoutToStderr():
+            dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1, device_id=device)
     keys, vals = bht.generate_unique_keys(SEED, rank * n, n, device=local)
     keys, vals = keys.view(torch.int32), vals.view(torch.int32)
     sharded = bht.ShardedTable(cfg, device=local, chunk=args.chunk)
@@ -547,8 +565,9 @@ def run_cuda(args):
         if marks is not None: marks.append(ev()); marks[-1].record(stream)
         return o
 
-    for _ in range(max(args.warmup, 3)):
-        o = step()
+    with StdoutToStderr():
+        for _ in range(max(args.warmup, 3)):
+            o = step()
     assert o.success, o
     assert torch.equal(out, vals), "sharded find answers differ from the inserted values"
     barrier()
@@ -644,7 +663,7 @@ def run_cuda(args):
                        "insert_probes_per_key": local_outcome.mean_probes, "find_probes_per_key": fs.mean_probes,
                        "exchange": "fixed segments, equal-split all_to_all_single, device-side counts; host reads per call: 1"},
         }
-        print(json.dumps(line))
+        print(json.dumps(line), flush=True)
     dist.destroy_process_group()
     return 0
 

@@ -84,12 +84,22 @@ struct Spill {
   uint2* pairs;
   uint32_t* start;
   unsigned long long* cursor;
+  unsigned long long cap;  // entries of the list (= the most pairs the build was announced to take)
+  DevCounters* ctr;        // a pair that does not even fit the list is dropped and reported as a failed insertion:
+  uint32_t* failed_keys;   // only a chunked build fed more pairs than it announced (device-counted chunks) gets there
+  uint64_t failed_cap;
 };
+
+__device__ __forceinline__ void spill_dropped(uint32_t key, const Spill& sp) {
+  atomicAdd(&sp.ctr->failed, 1ull);
+  record_failed(sp.ctr, sp.failed_keys, sp.failed_cap, key);
+}
 
 // A pair that found no room in a fixed-capacity segment / bin / stash goes to the spill list untouched (rare: the
 // capacities are mean + 6 sigma of a uniform hash; one global atomic per pair).
 __device__ __forceinline__ void spill_fresh(uint2 kv, const Spill& sp) {
   const unsigned long long pos = atomicAdd(sp.cursor, 1ull);
+  if (pos >= sp.cap) return spill_dropped(kv.x, sp);
   sp.pairs[pos] = kv;
   sp.start[pos] = kStartAtH0;
 }
@@ -564,8 +574,12 @@ region_build_kernel(const __grid_constant__ TableView t, uint32_t region_log2, u
       }
       // a hole (only on an uploaded store): the pair is simply placed; the reserved list entry becomes a tombstone
       if (vk == kEmptyKey) atomicAdd(&hole_count, 1u);
-      sp.pairs[stash_base + i] = make_uint2(vk, static_cast<uint32_t>(old >> 32));
-      sp.start[stash_base + i] = vk == kEmptyKey ? kStartTombstone : (next | 0x80000000u);
+      if (stash_base + i < sp.cap) {
+        sp.pairs[stash_base + i] = make_uint2(vk, static_cast<uint32_t>(old >> 32));
+        sp.start[stash_base + i] = vk == kEmptyKey ? kStartTombstone : (next | 0x80000000u);
+      } else if (vk != kEmptyKey) {
+        spill_dropped(vk, sp);  // the victim in hand is the pair dropped, as when a chain hits its cap
+      }
     }
   }
 #if BHT_BUILD_TMA_STORE
@@ -690,11 +704,11 @@ cudaError_t blocked_build_begin(const BlockedPlan& p, uint64_t n, void* scratch,
 }
 
 cudaError_t blocked_build_scatter(const TableView& t, const BlockedPlan& p, uint64_t n, void* scratch, const uint32_t* keys,
-                                  const uint32_t* values, uint64_t len, int sm_count, cudaStream_t stream,
+                                  const uint32_t* values, uint64_t len, const FailLog& log, int sm_count, cudaStream_t stream,
                                   const unsigned long long* len_dev) {
   if (len == 0) return cudaSuccess;
   const ScratchMap m = map_scratch(p, n, scratch);
-  const Spill sp{m.spill, m.spill_start, m.spill_cursor};
+  const Spill sp{m.spill, m.spill_start, m.spill_cursor, n, log.ctr, log.failed_keys, log.failed_cap};
   const bool aligned = ((reinterpret_cast<uintptr_t>(keys) | reinterpret_cast<uintptr_t>(values)) & 15) == 0;  // values may be null
   const uint32_t inv_per = static_cast<uint32_t>((1ull << 32) / p.per) + 1u;  // exact quotient for fine ids < 2^16, per <= 256
   const uint64_t tiles = (len + kSplitTile - 1) / kSplitTile;
@@ -709,10 +723,11 @@ cudaError_t blocked_build_scatter(const TableView& t, const BlockedPlan& p, uint
 }
 
 cudaError_t blocked_build_finish(const TableView& t, const BlockedPlan& p, uint64_t n, void* scratch, bool fresh,
-                                 DevCounters* ctr, int sm_count, cudaStream_t stream, PairSource* spill_out,
+                                 const FailLog& log, int sm_count, cudaStream_t stream, PairSource* spill_out,
                                  const unsigned long long** spill_count_out) {
+  DevCounters* ctr = log.ctr;
   const ScratchMap m = map_scratch(p, n, scratch);
-  const Spill sp{m.spill, m.spill_start, m.spill_cursor};
+  const Spill sp{m.spill, m.spill_start, m.spill_cursor, n, log.ctr, log.failed_keys, log.failed_cap};
   const uint64_t tiles_b = static_cast<uint64_t>(p.n_groups) * ((p.group_cap + kSplitTile - 1) / kSplitTile);
   const int grid_b = static_cast<int>(std::min<uint64_t>(tiles_b, static_cast<uint64_t>(sm_count) * BHT_SPLIT_CTAS));
   static const cudaError_t attr = cudaFuncSetAttribute(bin_split_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -742,11 +757,11 @@ cudaError_t blocked_build_finish(const TableView& t, const BlockedPlan& p, uint6
 }
 
 cudaError_t launch_blocked_build(const TableView& t, const BlockedPlan& p, const uint32_t* keys, const uint32_t* values,
-                                 uint64_t n, bool fresh, void* scratch, DevCounters* ctr, int sm_count, cudaStream_t stream,
+                                 uint64_t n, bool fresh, void* scratch, const FailLog& log, int sm_count, cudaStream_t stream,
                                  PairSource* spill_out, const unsigned long long** spill_count_out) {
   cudaError_t e = blocked_build_begin(p, n, scratch, stream);
-  if (e == cudaSuccess) e = blocked_build_scatter(t, p, n, scratch, keys, values, n, sm_count, stream);
-  if (e == cudaSuccess) e = blocked_build_finish(t, p, n, scratch, fresh, ctr, sm_count, stream, spill_out, spill_count_out);
+  if (e == cudaSuccess) e = blocked_build_scatter(t, p, n, scratch, keys, values, n, log, sm_count, stream, nullptr);
+  if (e == cudaSuccess) e = blocked_build_finish(t, p, n, scratch, fresh, log, sm_count, stream, spill_out, spill_count_out);
   return e;
 }
 

@@ -138,10 +138,12 @@ constexpr uint64_t kStageChunkMin = 1ull << 18;
 // Length of the staged chunk that starts at `off`: chunks double from kStageChunkMin up to kStageChunk and halve
 // again towards the end, so the pipeline fills and drains in ~1 MiB steps (the first copy-in and the last
 // kernel / copy-out are the only parts of a host-buffer call that nothing overlaps).
-uint64_t stage_chunk_len(uint64_t off, uint64_t n) {
+uint64_t stage_chunk_len(uint64_t off, uint64_t n, bool ramp_up = true) {
   const long v = knobs().stage_chunk_log2;
   const uint64_t chunk_max = 1ull << (v < 18 ? 18 : (v > 22 ? 22 : v));
-  const uint64_t up = std::max(kStageChunkMin, off);
+  // (no ramp-up when the device is still busy with an earlier call's work: nothing could start on a small first
+  // chunk anyway, and full-size chunks put three slots' worth of copies under that work)
+  const uint64_t up = ramp_up ? std::max(kStageChunkMin, off) : chunk_max;
   const uint64_t down = std::max(kStageChunkMin, (n - off) / 2);
   return std::min(std::min(chunk_max, n - off), std::min(up, down));
 }
@@ -249,6 +251,19 @@ bht_status validate_config(const bht_config& c) {
 }
 
 cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// SM count of a device, asked once (cudaGetDeviceProperties costs milliseconds per call: it was 8 ms of host time per
+// chunk of a sharded find).
+int device_sm_count(int device) {
+  static std::atomic<int> cached[64];
+  if (device < 0 || device >= 64) return 148;
+  int v = cached[device].load(std::memory_order_relaxed);
+  if (v == 0) {
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device) != cudaSuccess || v <= 0) v = 148;
+    cached[device].store(v, std::memory_order_relaxed);
+  }
+  return v;
+}
 
 bht_status ensure_staging(bht_table* t) {
   Staging& s = t->stage;
@@ -497,7 +512,8 @@ cudaError_t finish_blocked(bht_table* t, const BlockedPlan& plan, uint64_t n, vo
                            cudaStream_t stream) {
   PairSource spill{};
   const unsigned long long* spill_count = nullptr;
-  cudaError_t e = blocked_build_finish(t->view, plan, n, scratch, fresh, t->ctr, t->sm_count, stream, &spill, &spill_count);
+  cudaError_t e = blocked_build_finish(t->view, plan, n, scratch, fresh, FailLog{t->ctr, t->failed_keys, kFailedLogCap}, t->sm_count,
+                                       stream, &spill, &spill_count);
   if (e != cudaSuccess) return e;
   if (fused_fill) t->clear_pending.store(false, std::memory_order_release);  // the region build writes every slot of the store
   e = cudaEventRecord(t->phase_ev[1], stream);
@@ -548,7 +564,9 @@ bht_status do_insert(bht_table* t, const uint32_t* keys, const uint32_t* values,
       // first bucket was full (their count stays on the device).
       BHT_CUDA(scratch_alloc(t, &scratch.p, blocked_scratch_bytes(plan, n), stream));
       cudaError_t e = blocked_build_begin(plan, n, scratch.p, stream);
-      if (e == cudaSuccess) e = blocked_build_scatter(t->view, plan, n, scratch.p, keys, values, n, t->sm_count, stream);
+      if (e == cudaSuccess)
+        e = blocked_build_scatter(t->view, plan, n, scratch.p, keys, values, n, FailLog{t->ctr, t->failed_keys, kFailedLogCap},
+                                  t->sm_count, stream);
       if (e == cudaSuccess) e = finish_blocked(t, plan, n, scratch.p, t->known_empty, fused_fill, stream);
       if (e != cudaSuccess) return cuda_fail(e, "bht_insert (shared-memory blocked)");
       t->last_schedule = 3;
@@ -614,7 +632,7 @@ bht_status do_insert(bht_table* t, const uint32_t* keys, const uint32_t* values,
       BHT_CUDA(cudaStreamWaitEvent(st.compute, st.in_done[slot], 0));
       if (blocked) {
         BHT_CUDA(blocked_build_scatter(t->view, plan, n, scratch.p, st.keys[slot], derive ? nullptr : st.vals[slot], len,
-                                       t->sm_count, st.compute));
+                                       FailLog{t->ctr, t->failed_keys, kFailedLogCap}, t->sm_count, st.compute));
       } else {
         if (derive) BHT_CUDA(launch_derive_values(st.keys[slot], st.vals[slot], len, t->sm_count, st.compute));
         BHT_CUDA(launch_insert_kind(t, PairSource{st.keys[slot], st.vals[slot]}, len, 0, st.compute, false, nullptr,
@@ -678,13 +696,17 @@ bht_status session_feed(bht_table* t, const uint32_t* keys, const uint32_t* valu
   std::lock_guard<std::mutex> lock(t->mu);
   bht_table::Session& ses = t->session;
   if (!ses.active) return fail(BHT_INVALID_ARGUMENT, "bht_build_feed: no chunked build is open (bht_build_begin)");
-  if (ses.fed + n > ses.n_max) return fail(BHT_CAPACITY_EXCEEDED, "bht_build_feed: more pairs than bht_build_begin announced");
+  // a device-counted chunk only names an upper bound: what actually arrives beyond n_max is dropped and reported as
+  // failed insertions by the kernels (build_blocked.cu, Spill::cap)
+  if (n_dev == nullptr && ses.fed + n > ses.n_max)
+    return fail(BHT_CAPACITY_EXCEEDED, "bht_build_feed: more pairs than bht_build_begin announced");
   cudaStream_t stream = as_stream(stream_v);
   if (n == 0) return BHT_OK;
   if (n_dev != nullptr && !ses.blocked && t->cfg.kind != BHT_BCHT && t->cfg.kind != BHT_ONE_CHT)
     return fail(BHT_INVALID_ARGUMENT, "bht_build_feed_counted: device-side counts are for the cuckoo kinds");
   if (ses.blocked) {
-    BHT_CUDA(blocked_build_scatter(t->view, ses.plan, ses.n_max, ses.scratch, keys, values, n, t->sm_count, stream, n_dev));
+    BHT_CUDA(blocked_build_scatter(t->view, ses.plan, ses.n_max, ses.scratch, keys, values, n,
+                                   FailLog{t->ctr, t->failed_keys, kFailedLogCap}, t->sm_count, stream, n_dev));
   } else {
     BHT_CUDA(materialize_clear(t, stream));
     void* derived = nullptr;
@@ -779,9 +801,11 @@ bht_status do_find(const bht_table* ct, bool early_exit, const uint32_t* keys, u
     BHT_CUDA(cudaEventRecord(start, stream));
     BHT_CUDA(cudaStreamWaitEvent(st.compute, start, 0));
     uint64_t chunks = 0;
+    const bool device_idle = cudaEventQuery(t->build_done) == cudaSuccess;  // no host-buffer build still in flight
+    if (!device_idle) cudaGetLastError();
     for (uint64_t c = 0, off = 0; off < n; ++c) {
       const int slot = static_cast<int>(c % kStageSlots);
-      const uint64_t len = stage_chunk_len(off, n);
+      const uint64_t len = stage_chunk_len(off, n, device_idle);
       chunks = c + 1;
       // (also against the kernels of an earlier host-buffer insert, which returns before its device work is done)
       BHT_CUDA(cudaStreamWaitEvent(st.h2d, st.kernel_done[slot], 0));                       // keys[slot] consumed
@@ -1264,12 +1288,11 @@ bht_status bht_hash_keys(uint64_t alpha, uint64_t beta, uint64_t range, const ui
     return fail(BHT_INVALID_ARGUMENT, "bht_hash_keys: alpha, beta and range must fit 32 bits, range > 0");
   if (n != 0 && (keys == nullptr || out == nullptr)) return fail(BHT_INVALID_ARGUMENT, "bht_hash_keys: null argument");
   BHT_ON_DEVICE(device);
-  cudaDeviceProp prop;
-  BHT_CUDA(cudaGetDeviceProperties(&prop, device));
+  const int sm_count_dev = device_sm_count(device);
   const HashFn h = make_hash_fn(alpha, beta, range);
   cudaStream_t s = as_stream(stream);
   if (mem_space == BHT_MEM_DEVICE) {
-    BHT_CUDA(launch_hash_keys(h, keys, out, n, prop.multiProcessorCount, s));
+    BHT_CUDA(launch_hash_keys(h, keys, out, n, sm_count_dev, s));
     return BHT_OK;
   }
   if (n == 0) return BHT_OK;
@@ -1277,7 +1300,7 @@ bht_status bht_hash_keys(uint64_t alpha, uint64_t beta, uint64_t range, const ui
   BHT_CUDA(cudaMalloc(&dk, n * sizeof(uint32_t)));
   cudaError_t e = cudaMalloc(&dout, n * sizeof(uint32_t));
   if (e == cudaSuccess) e = cudaMemcpyAsync(dk, keys, n * sizeof(uint32_t), cudaMemcpyHostToDevice, s);
-  if (e == cudaSuccess) e = launch_hash_keys(h, dk, dout, n, prop.multiProcessorCount, s);
+  if (e == cudaSuccess) e = launch_hash_keys(h, dk, dout, n, sm_count_dev, s);
   if (e == cudaSuccess) e = cudaMemcpyAsync(out, dout, n * sizeof(uint32_t), cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   cudaFree(dk);
@@ -1302,15 +1325,14 @@ bht_status bht_shard_partition(uint64_t alpha, uint64_t beta, uint32_t n_shards,
   if (counts_host == nullptr || (n != 0 && (keys == nullptr || out_keys == nullptr)) || (values != nullptr && out_values == nullptr))
     return fail(BHT_INVALID_ARGUMENT, "bht_shard_partition: null argument");
   BHT_ON_DEVICE(device);
-  cudaDeviceProp prop;
-  BHT_CUDA(cudaGetDeviceProperties(&prop, device));
+  const int sm_count_dev = device_sm_count(device);
   cudaStream_t s = as_stream(stream);
   unsigned long long* scratch = nullptr;  // counts | cursors | n destination bytes
   BHT_CUDA(cudaMallocAsync(&scratch, 2 * sizeof(unsigned long long) * n_shards + n, s));
   const uint32_t a = static_cast<uint32_t>(alpha), b = static_cast<uint32_t>(beta);
   cudaError_t e = launch_shard_route(a, b, n_shards, keys, values, n, reinterpret_cast<uint8_t*>(scratch + 2 * n_shards), scratch,
                                      scratch + n_shards, out_keys, out_values,
-                                     out_index, prop.multiProcessorCount, s);
+                                     out_index, sm_count_dev, s);
   if (e == cudaSuccess) e = cudaMemcpyAsync(counts_host, scratch, sizeof(uint64_t) * n_shards, cudaMemcpyDeviceToHost, s);
   cudaFreeAsync(scratch, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
@@ -1331,13 +1353,7 @@ bht_status bht_shard_partition_fixed(uint64_t alpha, uint64_t beta, uint32_t n_s
       (values != nullptr && out_values == nullptr))
     return fail(BHT_INVALID_ARGUMENT, "bht_shard_partition_fixed: null argument");
   BHT_ON_DEVICE(device);
-  static int sm_counts[64] = {};
-  if (device < 64 && sm_counts[device] == 0) {
-    cudaDeviceProp prop;
-    BHT_CUDA(cudaGetDeviceProperties(&prop, device));
-    sm_counts[device] = prop.multiProcessorCount;
-  }
-  const int sm_count = device < 64 ? sm_counts[device] : 148;
+  const int sm_count = device_sm_count(device);
   cudaStream_t s = as_stream(stream);
   unsigned long long* scratch = nullptr;  // cursors | n destination bytes
   BHT_CUDA(cudaMallocAsync(&scratch, sizeof(unsigned long long) * n_shards + n + 16, s));
@@ -1355,9 +1371,8 @@ bht_status bht_shard_unpermute(const uint32_t* answers, const uint32_t* index, u
   if (n != 0 && (answers == nullptr || index == nullptr || out == nullptr))
     return fail(BHT_INVALID_ARGUMENT, "bht_shard_unpermute: null argument");
   BHT_ON_DEVICE(device);
-  cudaDeviceProp prop;
-  BHT_CUDA(cudaGetDeviceProperties(&prop, device));
-  BHT_CUDA(launch_unpermute(answers, index, n, out, prop.multiProcessorCount, as_stream(stream)));
+  const int sm_count_dev = device_sm_count(device);
+  BHT_CUDA(launch_unpermute(answers, index, n, out, sm_count_dev, as_stream(stream)));
   return BHT_OK;
 }
 
@@ -1369,9 +1384,8 @@ bht_status bht_generate_unique_keys(uint64_t seed, uint64_t offset, uint64_t n, 
   if (offset + n > 0xFFFFFFFFull || offset + n < offset)
     return fail(BHT_INVALID_ARGUMENT, "bht_generate_unique_keys: offset + n exceeds the 2^32 - 1 user keys");
   BHT_ON_DEVICE(device);
-  cudaDeviceProp prop;
-  BHT_CUDA(cudaGetDeviceProperties(&prop, device));
-  BHT_CUDA(launch_generate_keys(seed, offset, n, out_keys, out_values, prop.multiProcessorCount, as_stream(stream)));
+  const int sm_count_dev = device_sm_count(device);
+  BHT_CUDA(launch_generate_keys(seed, offset, n, out_keys, out_values, sm_count_dev, as_stream(stream)));
   return BHT_OK;
 }
 

@@ -63,22 +63,28 @@ struct BlockedPlan {
   uint32_t n_groups;     // groups (<= kMaxShards)
   uint32_t group_cap;    // pairs per group segment
 };
+// The counter block and the dropped-key log of the table (what the bulk-insert kernels report failures to).
+struct FailLog {
+  DevCounters* ctr;
+  uint32_t* failed_keys;
+  uint64_t failed_cap;
+};
 BlockedPlan plan_blocked_build(const TableView& t, uint64_t n);
 size_t blocked_scratch_bytes(const BlockedPlan& p, uint64_t n);
 // Places every pair whose H0 bucket has room; for the others the first eviction is done in place and the victim is
 // left in *spill_out (packed pairs + where their walk goes on, *spill_count_out of them, device pointers into
 // `scratch`) for launch_insert_cuckoo.
 cudaError_t launch_blocked_build(const TableView& t, const BlockedPlan& p, const uint32_t* keys, const uint32_t* values,
-                                 uint64_t n, bool fresh, void* scratch, DevCounters* ctr, int sm_count, cudaStream_t stream,
+                                 uint64_t n, bool fresh, void* scratch, const FailLog& log, int sm_count, cudaStream_t stream,
                                  PairSource* spill_out, const unsigned long long** spill_count_out);
 // The same build in steps, for a batch that arrives in chunks (n = the most pairs the chunks may add up to, the value
 // the plan and the scratch were sized for): begin, then scatter once per chunk (K8g), then finish (K10 + K11).
 cudaError_t blocked_build_begin(const BlockedPlan& p, uint64_t n, void* scratch, cudaStream_t stream);
 cudaError_t blocked_build_scatter(const TableView& t, const BlockedPlan& p, uint64_t n, void* scratch, const uint32_t* keys,
-                                  const uint32_t* values, uint64_t len, int sm_count, cudaStream_t stream,
+                                  const uint32_t* values, uint64_t len, const FailLog& log, int sm_count, cudaStream_t stream,
                                   const unsigned long long* len_dev = nullptr);  // when set: min(len, *len_dev) pairs, read on the device
 cudaError_t blocked_build_finish(const TableView& t, const BlockedPlan& p, uint64_t n, void* scratch, bool fresh,
-                                 DevCounters* ctr, int sm_count, cudaStream_t stream, PairSource* spill_out,
+                                 const FailLog& log, int sm_count, cudaStream_t stream, PairSource* spill_out,
                                  const unsigned long long** spill_count_out);
 
 // util.cu — K0 fill, K7 count, admissibility, hash hook, K8/K9 shard routing, synthetic keys.

@@ -131,8 +131,14 @@ class CudaShardOps:
         _check(self._lib.bht_build_feed_counted(self.table._h, keys.data_ptr(), values.data_ptr(), cap, count.data_ptr(),
                                                 _stream_ptr(None, self.device)))
 
+    def build_feed(self, keys: torch.Tensor, values: torch.Tensor) -> None:
+        self.table.build_feed(keys, values)
+
     def build_end(self) -> BuildOutcome:
         return self.table.build_end()
+
+    def find_into(self, keys: torch.Tensor, out: torch.Tensor) -> None:
+        self.table.find(keys, out)
 
     def find(self, keys: torch.Tensor) -> torch.Tensor:
         out = self.empty(keys.numel())
@@ -231,6 +237,13 @@ class ShardedTable:
         """Routes this rank's (key, value) pairs to their owners and bulk-inserts what this rank owns.
         Returns the outcome aggregated over all ranks."""
         keys, values = self._i32(keys), self._i32(values)
+        if self.world == 1 and exact is None and hasattr(self.ops, "build_feed"):
+            # one shard owns every key: nothing to route, the chunks go straight into the chunked build
+            self.ops.build_begin(self.cfg.capacity)
+            for lo, hi in self._chunks(keys.numel()):
+                self.ops.build_feed(keys[lo:hi], values[lo:hi])
+            o = self.ops.build_end()
+            return self._aggregate([o.attempted, o.inserted, o.failed, o.probes], o.failed_key)
         if self._use_exact(exact):
             return self._insert_exact(keys, values)
         chunks = self._chunks(keys.numel())
@@ -298,6 +311,10 @@ class ShardedTable:
         keys = self._i32(keys)
         n = keys.numel()
         out = self.ops.empty(n) if out is None else self._i32(out)
+        if self.world == 1 and exact is None and hasattr(self.ops, "find_into"):
+            for lo, hi in self._chunks(n):
+                self.ops.find_into(keys[lo:hi], out[lo:hi])
+            return out
         if self._use_exact(exact):
             return self._find_exact(keys, out)
         chunks = self._chunks(n)

@@ -28,7 +28,7 @@ def nccl_world():
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("exact", [False, True])
+@pytest.mark.parametrize("exact", [None, False, True])  # None: a world of one needs no routing at all
 @pytest.mark.parametrize("chunk", [1 << 26, 100_000])
 def test_sharded_table_world_of_one(bht, nccl_world, chunk, exact):
     n = 700_000
@@ -62,14 +62,16 @@ def test_sharded_build_in_chunks_takes_the_blocked_build(bht, nccl_world):
     keys, vals = keys.view(torch.int32), vals.view(torch.int32)
     cfg = bht.make_config("bcht", n, 0.9, 16, seed=bht.mix_seed(1, 0x100))
     st = bht.ShardedTable(cfg, device=0, chunk=1 << 22)
-    launches0 = bht.kernel_launch_count()
-    o = st.insert(keys, vals)
-    assert o.success and o.inserted == n
-    assert st.ops.table.last_build_schedule() == 3
-    # 8 chunks: route (3 kernels) + one first-pass launch per chunk, then K10, K11, K4 once
-    assert bht.kernel_launch_count() - launches0 <= 8 * 4 + 3 + 2
-    out = st.find(keys)
-    assert torch.equal(out, vals)
+    for exact in (False, None):  # the routed exchange (as N > 1 runs it), then the no-routing shortcut of a world of one
+        st.ops.table.clear()
+        launches0 = bht.kernel_launch_count()
+        o = st.insert(keys, vals, exact=exact)
+        assert o.success and o.inserted == n
+        assert st.ops.table.last_build_schedule() == 3
+        # 8 chunks: route (3 kernels) + one first-pass launch per chunk, then K10, K11, K4 once
+        assert bht.kernel_launch_count() - launches0 <= 8 * 4 + 3 + 2
+        out = st.find(keys, exact=exact)
+        assert torch.equal(out, vals)
     plain = bht.HashTable(cfg, 0)
     assert plain.insert(keys, vals).success and plain.last_build_schedule() == 3
     _, fa = st.ops.table.find(keys, want_stats=True)
