@@ -115,6 +115,7 @@ SIGNATURES = {
     "bht_set_blocked_insert": (C.c_int, [_vp, C.c_int32]),
     "bht_last_build_schedule": (C.c_int32, [_vp]),
     "bht_set_tail_throttle": (C.c_int, [_vp, C.c_int32]),
+    "bht_set_repair": (C.c_int, [_vp, C.c_int32]),
     "bht_last_insert_phases": (C.c_int, [_vp, C.POINTER(C.c_float), C.POINTER(C.c_float)]),
     "bht_load_factor": (C.c_int, [_vp, _u64p, _u64p]),
     "bht_count_occupied": (C.c_int, [_vp, _u64p, _vp]),

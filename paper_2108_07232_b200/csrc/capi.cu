@@ -148,6 +148,7 @@ uint64_t stage_chunk_len(uint64_t off, uint64_t n, bool ramp_up = true) {
   return std::min(std::min(chunk_max, n - off), std::min(up, down));
 }
 constexpr uint64_t kFailedLogCap = 1ull << 20;
+constexpr uint32_t kMaxRepair = 256;  // dropped pairs of one launch that get a second, solitary insertion (insert_cuckoo.cu)
 constexpr uint32_t kRetryCap = 1024;
 
 // Host <-> device staging for BHT_MEM_HOST calls: kStageSlots chunks in flight, copy-in, probe kernel
@@ -200,6 +201,7 @@ struct bht_table {
   } session;
   uint64_t host_inserted = 0;  // upper bound of the pairs in the store, kept on the host (tail_plan)
   bool tail_throttle = false;  // bht_set_tail_throttle
+  bool repair_dropped = true;  // bht_set_repair: cuckoo kinds, see repair_dropped_kernel (insert_cuckoo.cu)
   // bp2ht / iht: one 32-bit load counter per bucket for the counter-claimed insert (insert_claim.cu); loads_valid =
   // the counters describe the store (false after anything else may have written slots: they are rebuilt on demand)
   uint32_t* loads = nullptr;
@@ -331,6 +333,7 @@ cudaError_t launch_insert_kind(bht_table* t, PairSource src, uint64_t n, int max
   a.ctr = t->ctr;
   a.failed_keys = t->failed_keys;
   a.failed_cap = kFailedLogCap;
+  a.max_repair = t->repair_dropped ? kMaxRepair : 0u;
   a.sm_count = t->sm_count;
   a.max_ctas_per_sm = max_ctas_per_sm;
   const Knobs& k = knobs();
@@ -946,7 +949,7 @@ bht_status bht_create(const bht_config* cfg, int32_t device, bht_table** out) {
   if (e == cudaSuccess) e = cudaMalloc(&store, cfg->capacity * sizeof(uint64_t));  // cudaMalloc aligns to >= 256 B
   if (e == cudaSuccess) e = cudaMalloc(&t->ctr, sizeof(DevCounters));
   if (e == cudaSuccess) e = cudaMallocHost(&t->ctr_host, sizeof(DevCounters));
-  if (e == cudaSuccess) e = cudaMalloc(&t->failed_keys, kFailedLogCap * sizeof(uint32_t));
+  if (e == cudaSuccess) e = cudaMalloc(&t->failed_keys, 2 * kFailedLogCap * sizeof(uint32_t));  // keys, then values
   if (e == cudaSuccess) e = cudaMalloc(&t->cursors, kCursorSlots * sizeof(uint32_t));
   for (int i = 0; i < 3 && e == cudaSuccess; ++i) e = cudaEventCreate(&t->phase_ev[i]);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&t->fill_done, cudaEventDisableTiming);
@@ -1150,6 +1153,12 @@ bht_status bht_set_iht_prose_fallback(bht_table* t, int32_t enabled) {
   if (t == nullptr) return fail(BHT_INVALID_ARGUMENT, "bht_set_iht_prose_fallback: null table");
   if (t->cfg.kind != BHT_IHT) return fail(BHT_KIND_MISMATCH, "iht_insert: table kind does not match the variant");
   t->view.prose = enabled ? 1u : 0u;
+  return BHT_OK;
+}
+
+bht_status bht_set_repair(bht_table* t, int32_t enabled) {
+  if (t == nullptr) return fail(BHT_INVALID_ARGUMENT, "bht_set_repair: null table");
+  t->repair_dropped = enabled != 0;
   return BHT_OK;
 }
 

@@ -6,9 +6,15 @@ namespace bht_b200 {
 
 // Appends a dropped key to the table's failed-key log (the GPU image of build_outcome::failed_key,
 // reference: proj/include/bht/table.hpp:115-120; a bulk insert can drop more than one).
-__device__ __forceinline__ void record_failed(DevCounters* ctr, uint32_t* failed_keys, uint64_t failed_cap, uint32_t key) {
+// The log holds failed_cap keys followed by failed_cap values (the value of a dropped pair lets the cuckoo repair pass,
+// insert_cuckoo.cu, insert it once more).
+__device__ __forceinline__ void record_failed(DevCounters* ctr, uint32_t* failed_keys, uint64_t failed_cap, uint32_t key,
+                                              uint32_t value = 0u) {
   const unsigned long long pos = atomicAdd(&ctr->failed_recorded, 1ull);
-  if (pos < failed_cap) failed_keys[pos] = key;
+  if (pos < failed_cap) {
+    failed_keys[pos] = key;
+    failed_keys[failed_cap + pos] = value;
+  }
   atomicMax(&ctr->failed_key_tag, key + 1u);
 }
 

@@ -122,14 +122,14 @@ bulk_insert_cuckoo_kernel(const __grid_constant__ TableView t, const PairSource 
           have = false;
         } else if (++retries > t.retry_cap) {
           ++n_fail;
-          record_failed(ctr, failed_keys, failed_cap, key);
+          record_failed(ctr, failed_keys, failed_cap, key, val);
           have = false;
         } else {
           hint = load + 1;  // lost the slot
         }
       } else if (dropped) {
         ++n_fail;
-        record_failed(ctr, failed_keys, failed_cap, key);  // the pair in hand is the one dropped
+        record_failed(ctr, failed_keys, failed_cap, key, val);  // the pair in hand is the one dropped
         have = false;
       } else if (evict) {
         const uint32_t vk = static_cast<uint32_t>(got_e);
@@ -162,6 +162,81 @@ bulk_insert_cuckoo_kernel(const __grid_constant__ TableView t, const PairSource 
   flush_insert_counters(ctr, lane, n_ins, n_fail, n_probe);
 }
 
+// ---- repair pass ------------------------------------------------------------------------------------------------
+// The reference inserts one pair at a time: an eviction chain never meets another walker, and max_chain
+// (core.cpp:28-31) is calibrated for that.  A bulk build has ~190 k walkers in flight; near the end of a build at load
+// factor 0.99 they are as many as the free slots that remain, take the slots each other was heading for, and hit
+// max_chain 3-5 times more often — 50 % of such builds dropped one to three pairs where the reference's build fails
+// 10 % of the time (profiles/r01j_*).  So the (few) pairs a launch dropped are inserted ONCE MORE here, by a single
+// thread, one after the other, with nobody else moving pairs: the insertion loop of table.cpp:53-92 verbatim, a fresh
+// chain of at most max_chain evictions, cap tested before the exchange, lowest-index rotation.  A pair that fails
+// again stays failed.  More than `max_repair` dropped pairs means the table is simply over-full: nothing is repaired.
+template <int B, int H>
+__global__ void repair_dropped_kernel(const __grid_constant__ TableView t, DevCounters* __restrict__ ctr,
+                                      uint32_t* __restrict__ failed_keys, uint64_t failed_cap, uint32_t max_repair) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const unsigned long long n_fail = ctr->failed;  // this call's drops: the last n_fail entries of the log
+  const unsigned long long end = ctr->failed_recorded;
+  if (n_fail == 0 || n_fail > max_repair || end > failed_cap || n_fail > end) return;
+  const unsigned long long first = end - n_fail;
+  volatile unsigned long long* store = reinterpret_cast<volatile unsigned long long*>(t.store);
+  uint64_t rng = xorshift_init(mix_seed(t.seed, 0x72657072ull));
+  unsigned long long kept = 0, probes = 0;
+  uint32_t tag = 0;
+  for (unsigned long long i = first; i < end; ++i) {
+    uint32_t key = failed_keys[i], val = failed_keys[failed_cap + i];
+    uint32_t bid = bucket_index(t.h[0], key), chain = 0;
+    bool placed = false;
+    for (;;) {
+      ++probes;
+      volatile unsigned long long* bucket = store + static_cast<uint64_t>(bid) * B;
+      uint32_t load = 0;
+      while (load < B && static_cast<uint32_t>(bucket[load]) != kEmptyKey) ++load;  // first empty slot = the load (occupied slots form a prefix)
+      if (load < B) {
+        bucket[load] = pack_pair(key, val);
+        placed = true;
+        break;
+      }
+      if (chain >= t.max_chain) break;  // cap checked BEFORE the exchange (table.cpp:67)
+      const uint32_t slot = xorshift_next_below(rng, B);
+      const unsigned long long old = bucket[slot];
+      bucket[slot] = pack_pair(key, val);
+      key = static_cast<uint32_t>(old);
+      val = static_cast<uint32_t>(old >> 32);
+      uint32_t cand[H];
+#pragma unroll
+      for (int h = 0; h < H; ++h) cand[h] = bucket_index(t.h[h], key);
+      uint32_t next = cand[0];
+#pragma unroll
+      for (int h = H - 1; h >= 0; --h)  // lowest matching index wins (table.cpp:74-80)
+        if (cand[h] == bid) next = cand[(h + 1) % H];
+      bid = next;
+      ++chain;
+    }
+    if (!placed) {  // the pair in hand now is the one dropped
+      failed_keys[first + kept] = key;
+      failed_keys[failed_cap + first + kept] = val;
+      ++kept;
+      tag = max(tag, key + 1u);
+    }
+  }
+  const unsigned long long repaired = n_fail - kept;
+  ctr->failed = kept;
+  ctr->failed_recorded = first + kept;
+  ctr->failed_key_tag = tag;
+  ctr->inserted += repaired;
+  ctr->inserted_total += repaired;
+  ctr->insert_probes += probes;
+}
+
+template <int B, int H>
+static cudaError_t launch_repair(const TableView& t, const InsertLaunch& a) {
+  if (a.max_repair == 0) return cudaSuccess;
+  repair_dropped_kernel<B, H><<<1, 32, 0, a.stream>>>(t, a.ctr, a.failed_keys, a.failed_cap, a.max_repair);
+  note_launch();
+  return cudaGetLastError();
+}
+
 template <int B, int H>
 static cudaError_t launch_one(const TableView& t, const InsertLaunch& a) {
   if constexpr (B >= 4 && B <= 16) {
@@ -172,7 +247,8 @@ static cudaError_t launch_one(const TableView& t, const InsertLaunch& a) {
       if (a.max_grid > 0 && grid > a.max_grid) grid = a.max_grid;
       kernel<<<grid, block, 0, a.stream>>>(t, a.src, a.n, a.n_dev, a.routed, a.ctr, a.failed_keys, a.failed_cap, a.work_cursor);
       note_launch();
-      return cudaGetLastError();
+      const cudaError_t e = cudaGetLastError();
+      return e != cudaSuccess ? e : launch_repair<B, H>(t, a);
     }
   }
   auto kernel = bulk_insert_cuckoo_kernel<B, H, false>;
@@ -182,7 +258,8 @@ static cudaError_t launch_one(const TableView& t, const InsertLaunch& a) {
   if (a.max_grid > 0 && grid > a.max_grid) grid = a.max_grid;
   kernel<<<grid, block, smem, a.stream>>>(t, a.src, a.n, a.n_dev, a.routed, a.ctr, a.failed_keys, a.failed_cap, a.work_cursor);
   note_launch();
-  return cudaGetLastError();
+  const cudaError_t e = cudaGetLastError();
+  return e != cudaSuccess ? e : launch_repair<B, H>(t, a);
 }
 
 cudaError_t launch_insert_cuckoo(const TableView& t, const InsertLaunch& a) {

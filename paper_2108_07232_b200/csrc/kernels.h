@@ -29,8 +29,9 @@ struct InsertLaunch {
   PairSource src;
   uint64_t n;
   DevCounters* ctr;
-  uint32_t* failed_keys;  // dropped-key log and its capacity
+  uint32_t* failed_keys;  // dropped-pair log (failed_cap keys, then failed_cap values) and its capacity
   uint64_t failed_cap;
+  uint32_t max_repair = 0;  // cuckoo: after the launch, up to this many dropped pairs are inserted once more, one at a time
   uint32_t* work_cursor;  // one zeroed device word per launch (Stream)
   int sm_count;
   int max_ctas_per_sm;    // 0 = whatever fits; a routed (L2-blocked) build keeps fewer keys in flight

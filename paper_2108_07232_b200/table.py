@@ -379,6 +379,11 @@ class HashTable:
         return BuildOutcome(bool(res.success), res.inserted, res.failed, res.attempted, res.probes,
                             None if res.first_failed_key == EMPTY_KEY else res.first_failed_key)
 
+    def set_repair(self, enabled: bool) -> None:
+        """cuckoo kinds: the few pairs a launch dropped at the chain cap are inserted once more, one at a time, as the
+        reference inserts every pair (on by default; off = the raw outcome of the concurrent walks)."""
+        _check(self._lib.bht_set_repair(self._h, int(bool(enabled))))
+
     def set_tail_throttle(self, enabled: bool) -> None:
         """cuckoo kinds: insert the pairs that arrive beyond load 0.98 with few keys in flight — build success at load
         factor 0.99 closer to the reference's (~80 % instead of ~50 %; reference 90 %) for 2.5x the build time.  Off by

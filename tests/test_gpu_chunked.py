@@ -190,3 +190,38 @@ def test_deferred_fill_is_ordered_across_streams(bht):
         assert int((b.view(torch.int32) != -1).sum()) == 0, "a find on another stream read the store before the deferred fill"
         del junk
     table.close()
+
+
+def test_build_success_at_load_099_matches_the_reference(bht, ref):
+    """build_outcome.success at the edge of the load range.  The reference inserts one pair at a
+    time; its build of 10^6 keys at load factor 0.99 succeeds ~9 times in 10 (max_chain = 140, core.cpp:28-31).  The
+    concurrent walks of a bulk build alone succeed about half the time (set_repair(False)); with the repair pass — the
+    dropped pairs inserted once more, one at a time — the success count over the same seeds must not fall short of the
+    reference's own (experiments.cpp:110-140 counts successes per load factor in the same way)."""
+    n, seeds = 1_000_000, 40
+    keys = unique_keys(n, 2024)
+    d_keys = dev(keys)
+    ref_ok = gpu_ok = raw_ok = 0
+    for s in range(seeds):
+        cfg = bht.make_config("bcht", n, 0.99, 16, seed=bht.mix_seed(900 + s, 0x100))
+        rt, out = ref.build(keys, to_oracle_cfg(cfg))
+        ref_ok += bool(out["success"])
+        rt.close()
+        for repair in (True, False):
+            table = bht.HashTable(cfg, 0)
+            table.set_repair(repair)
+            o = table.insert(d_keys)
+            assert o.attempted == n and o.inserted + o.failed == n
+            assert table.occupied_slots() == o.inserted and table.count_inadmissible() == 0
+            if o.success:
+                assert int((table.find(d_keys).view(torch.int32) == -1).sum()) == 0
+            else:
+                assert len(table.failed_keys()) == o.failed
+            if repair:
+                gpu_ok += o.success
+            else:
+                raw_ok += o.success
+            table.close()
+    print(f"success at LF 0.99 over {seeds} seeds: reference {ref_ok}, gpu with repair {gpu_ok}, concurrent walks alone {raw_ok}")
+    assert gpu_ok >= ref_ok - 3, (ref_ok, gpu_ok, raw_ok)
+    assert gpu_ok >= raw_ok
