@@ -27,8 +27,11 @@ CELLS = [
     ("bcht", 16, 0.99, None, (1.4223, 1.3924, 2.7984)),
     ("1cht", 1, 0.8, None, (2.0554, 1.9214, 2.9513)),
     ("1cht", 1, 0.9, None, (2.7538, 2.2572, 3.4380)),
+    ("bp2ht", 16, 0.6, None, (2.0, 1.3265, 2.0)),
     ("bp2ht", 16, 0.8, None, (2.0, 1.33, 2.0)),
+    ("bp2ht", 16, 0.82, None, (2.0, 1.3303, 2.0)),  # the last load factor every 50 M-key build reaches (success curve, profiles/)
     ("iht", 16, 0.8, None, (1.3757, 1.2593, 3.0)),
+    ("iht", 16, 0.86, 12, (1.4818, 1.3308, 3.0)),
 ]
 
 
@@ -64,4 +67,38 @@ def test_full_size_properties(bht, workload, kind, b, lf, t, ref_probes):
     if kind in ("bcht", "1cht"):
         q = half[:: N // (1 << 22)].contiguous()
         assert torch.equal(table.find(q), table.find_exhaustive(q))
+    table.close()
+
+
+# BASELINE.json configs 3 and 4 beyond what the stable tables can hold: the reference's build() of the same cell fails
+# too (bp2ht b=16 holds ~0.84, iht b=16 t=12 ~0.86: acceptance.cpp:214-240).  A bulk insert attempts every pair and
+# reports the ones it dropped; expected dropped fractions from the reference's sequential insert_pair loop at 10^6 keys.
+FAILING = [("bp2ht", 16, 0.9, None, 8.6e-5), ("iht", 16, 0.9, 12, 1.3e-5), ("iht", 16, 0.99, 12, 1.04e-2)]
+
+
+@pytest.mark.parametrize("kind,b,lf,t,ref_drop", FAILING)
+def test_full_size_cells_that_do_not_build(bht, workload, kind, b, lf, t, ref_drop):
+    """The failed-build contract (tests/test_gpu_edge.py) at 50 M keys: attempted = inserted + failed, the store holds
+    exactly the inserted pairs, all admissible, every stored key answers with its value, every dropped key is absent,
+    and the dropped fraction is the reference's."""
+    present, absent, values, _ = workload
+    cfg = bht.make_config(kind, N, lf, b, threshold=t, seed=bht.mix_seed(3, 0x100))
+    table, o = bht.build(present, cfg, values, device=0)
+    assert not o.success and o.attempted == N and o.inserted + o.failed == N and o.failed > 0
+    assert table.inserted() == o.inserted == table.occupied_slots() and table.count_inadmissible() == 0
+    out = torch.empty(N, dtype=torch.int32, device="cuda")
+    _, st = table.find(present, out, want_stats=True)
+    found = out != -1
+    assert st.hits == o.inserted == int(found.sum()) and torch.equal(out[found], values[found])
+    drop = o.failed / N
+    assert 0.5 * ref_drop <= drop <= 2.0 * ref_drop + 2e-6, (drop, ref_drop)
+    if o.failed <= 1 << 20:
+        dropped = torch.from_numpy(table.failed_keys().view(np.int32)).cuda()
+        assert dropped.numel() == o.failed
+        assert bool((table.find(dropped).view(torch.int32) == -1).all())
+        assert torch.equal(torch.sort(dropped).values, torch.sort(present[~found]).values)
+    _, st0 = table.find(absent, out, want_stats=True)
+    assert st0.hits == 0
+    if kind == "bp2ht":
+        assert o.probes == 2 * N  # two probes per attempt, placed or not (table.cpp:109-130)
     table.close()
