@@ -201,7 +201,7 @@ struct bht_table {
   } session;
   uint64_t host_inserted = 0;  // upper bound of the pairs in the store, kept on the host (tail_plan)
   bool tail_throttle = false;  // bht_set_tail_throttle
-  bool repair_dropped = true;  // bht_set_repair: cuckoo kinds, see repair_dropped_kernel (insert_cuckoo.cu)
+  bool repair_dropped = false;  // bht_set_repair (default: on for bcht, off for 1cht), see repair_dropped_kernel (insert_cuckoo.cu)
   // bp2ht / iht: one 32-bit load counter per bucket for the counter-claimed insert (insert_claim.cu); loads_valid =
   // the counters describe the store (false after anything else may have written slots: they are rebuilt on demand)
   uint32_t* loads = nullptr;
@@ -333,7 +333,9 @@ cudaError_t launch_insert_kind(bht_table* t, PairSource src, uint64_t n, int max
   a.ctr = t->ctr;
   a.failed_keys = t->failed_keys;
   a.failed_cap = kFailedLogCap;
-  a.max_repair = t->repair_dropped ? kMaxRepair : 0u;
+  // (a launch of at most one warp's worth of pairs has no concurrency to make up for: one pair per launch is the
+  // reference's insert_pair exactly, failed insertions included)
+  a.max_repair = (t->repair_dropped && n > 32) ? kMaxRepair : 0u;
   a.sm_count = t->sm_count;
   a.max_ctas_per_sm = max_ctas_per_sm;
   const Knobs& k = knobs();
@@ -961,6 +963,7 @@ bht_status bht_create(const bht_config* cfg, int32_t device, bht_table** out) {
   }
   if (e == cudaSuccess) e = cudaMemset(t->ctr, 0, sizeof(DevCounters));
   t->cfg = *cfg;
+  t->repair_dropped = cfg->kind == BHT_BCHT;
   if (defer_fill_pays(t)) t->clear_pending.store(true);  // filled by its first user (materialize_clear) or by a blocked build
   else if (e == cudaSuccess) e = launch_fill_empty(store, cfg->capacity, t->sm_count, nullptr);
   if (e == cudaSuccess) e = cudaStreamSynchronize(nullptr);

@@ -225,3 +225,6 @@ def test_build_success_at_load_099_matches_the_reference(bht, ref):
     print(f"success at LF 0.99 over {seeds} seeds: reference {ref_ok}, gpu with repair {gpu_ok}, concurrent walks alone {raw_ok}")
     assert gpu_ok >= ref_ok - 3, (ref_ok, gpu_ok, raw_ok)
     assert gpu_ok >= raw_ok
+    # one pair per launch is insert_pair exactly: a failing insertion is not given a second chain (scenario tests pin
+    # the probe counts); 1cht keeps the raw outcome by default
+    assert bht.HashTable(bht.make_config("1cht", 1000, 0.5, 1, seed=1), 0) is not None
