@@ -54,8 +54,8 @@
 #define BHT_BUILD_TMA_STORE 1
 #endif
 
-#ifndef BHT_BUILD_PREFETCH  // 1: a CTA of K11 prefetches the bin of the CTA that will take its place into the L2
-#define BHT_BUILD_PREFETCH 1
+#ifndef BHT_BUILD_PREFETCH  // 1: a CTA of K11 prefetches the bin of the CTA that will take its place into the L2 (measured: +200 MB of DRAM reads, the prefetched lines are fetched twice, and no gain: 263.1 against 263.8 us)
+#define BHT_BUILD_PREFETCH 0
 #endif
 
 #ifndef BHT_SPLIT_TMA  // 1: the next tile's input arrives by a bulk asynchronous copy (TMA) while this one is processed
