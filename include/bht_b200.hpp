@@ -176,6 +176,28 @@ class hash_table {
     check(bht_last_insert_result(h_, &r, stream));
     return outcome_of(r);
   }
+  // build() with the key set handed over in device-resident chunks (table.cpp:231-271): at most n_max pairs between
+  // build_begin and build_end; values == nullptr pairs every key with value_for_key(key).  A table that qualifies for
+  // the shared-memory-blocked build takes each chunk through its first partition pass as it is fed.
+  void build_begin(std::uint64_t n_max, void* stream = nullptr) { check(bht_build_begin(h_, n_max, stream)); }
+  void build_feed(const key_type* device_keys, const value_type* device_values, std::uint64_t n, void* stream = nullptr) {
+    check(bht_build_feed(h_, device_keys, device_values, n, stream));
+  }
+  // the chunk holds min(n_cap, *n_device) pairs, the count read on the device (receive side of a sync-free exchange)
+  void build_feed_counted(const key_type* device_keys, const value_type* device_values, std::uint64_t n_cap,
+                          const std::uint64_t* n_device, void* stream = nullptr) {
+    check(bht_build_feed_counted(h_, device_keys, device_values, n_cap, n_device, stream));
+  }
+  build_outcome build_end(void* stream = nullptr) {
+    bht_insert_result r{};
+    check(bht_build_end(h_, &r, stream));
+    return outcome_of(r);
+  }
+  // 0 = caller order, 2 = L2-routed, 3 = shared-memory-blocked: how the last insert / chunked build ran
+  int last_build_schedule() const { return bht_last_build_schedule(h_); }
+  // cuckoo kinds: the few pairs a concurrent launch dropped at the chain cap get one more, solitary insertion
+  // (default: on for bcht, off for 1cht)
+  void set_repair(bool on) { check(bht_set_repair(h_, on ? 1 : 0)); }
   std::vector<key_type> failed_keys(std::uint64_t max_keys = 1u << 20) {
     std::vector<key_type> out(max_keys);
     std::uint64_t count = 0;

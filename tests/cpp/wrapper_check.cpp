@@ -10,6 +10,8 @@
 #include <algorithm>
 #include <vector>
 
+#include <cuda_runtime_api.h>  // device buffers for the chunked build (the library links its own static runtime)
+
 #include "bht_b200.hpp"
 
 using namespace bht::gpu;
@@ -224,6 +226,29 @@ int main(int argc, char** argv) {
       t.find(keys.data(), out.data(), n);
       CHECK(out == vals);
     }
+  }
+  // the chunked build through the C++ layer: host keys copied to the device in three pieces, fed, ended
+  {
+    table_config cfg = make_config(table_kind::bcht, n, 0.9, 16, std::nullopt, 10);
+    hash_table t(cfg);
+    t.set_blocked_insert(3);
+    t.set_repair(true);
+    std::vector<value_type> vals(n), out(n);
+    for (std::uint64_t i = 0; i < n; ++i) vals[i] = value_for_key(keys[i]);
+    key_type* dk = nullptr;
+    CHECK(cudaMalloc(reinterpret_cast<void**>(&dk), n * sizeof(key_type)) == cudaSuccess);
+    CHECK(cudaMemcpy(dk, keys.data(), n * sizeof(key_type), cudaMemcpyHostToDevice) == cudaSuccess);
+    t.build_begin(n);
+    CHECK(throws<std::invalid_argument>([&] { t.insert(keys.data(), vals.data(), 4); }));  // a chunked build is open
+    const std::uint64_t cut1 = n / 3, cut2 = n / 2 + 1;
+    t.build_feed(dk, nullptr, cut1);
+    t.build_feed(dk + cut1, nullptr, cut2 - cut1);
+    t.build_feed(dk + cut2, nullptr, n - cut2);
+    build_outcome o = t.build_end();
+    CHECK(o.success && o.inserted == n && t.last_build_schedule() == 3 && t.count_inadmissible() == 0);
+    t.find(keys.data(), out.data(), n);
+    CHECK(out == vals);
+    cudaFree(dk);
   }
   std::puts("wrapper checks ok");
   return 0;

@@ -13,8 +13,10 @@ LIBDIR = os.path.join(ROOT, "paper_2108_07232_b200", "lib")
 
 def build_exe(tmpdir):
     exe = os.path.join(tmpdir, "wrapper_check")
-    subprocess.check_call(["g++", "-std=c++17", "-O1", "-I" + os.path.join(ROOT, "include"), SRC, "-o", exe, "-L" + LIBDIR,
-                           "-lbht_b200", "-Wl,-rpath," + LIBDIR])
+    cuda = os.environ.get("CUDA_HOME", "/usr/local/cuda")
+    subprocess.check_call(["g++", "-std=c++17", "-O1", "-I" + os.path.join(ROOT, "include"), "-I" + os.path.join(cuda, "include"),
+                           SRC, "-o", exe, "-L" + LIBDIR, "-lbht_b200", "-L" + os.path.join(cuda, "lib64"), "-lcudart",
+                           "-Wl,-rpath," + LIBDIR, "-Wl,-rpath," + os.path.join(cuda, "lib64")])
     return exe
 
 
