@@ -22,6 +22,7 @@ while time.time() - t0 < budget:
     mode = int(rng.choice([0, 1, 2, 3]))
     n_batches = int(rng.choice([1, 1, 2, 3]))
     throttle = bool(rng.integers(0, 2))
+    how = str(rng.choice(["bulk", "bulk", "chunked", "host"]))  # bht_insert per batch / one chunked build / host arrays
     raw = np.unique(rng.integers(0, 0xFFFFFFFF, size=2 * n + 64, dtype=np.uint64).astype(np.uint32))
     rng.shuffle(raw)
     keys, absent = raw[:n], raw[n:n + min(n, 5000) + 1]
@@ -36,13 +37,24 @@ while time.time() - t0 < budget:
     cuts = sorted(set([0, n] + [int(x) for x in rng.integers(0, n + 1, size=n_batches - 1)]))
     off = int(rng.integers(0, 4))  # unaligned device slices
     inserted = failed = 0
+    if how == "chunked":
+        table.build_begin(n)
     for lo, hi in zip(cuts[:-1], cuts[1:]):
-        dk = dev(np.concatenate([np.zeros(off, np.uint32), keys[lo:hi]]))[off:]
-        dv = dev(np.concatenate([np.zeros(off, np.uint32), vals[lo:hi]]))[off:]
-        o = table.insert(dk, dv)
+        if how == "host":
+            o = table.insert(keys[lo:hi], vals[lo:hi])
+        else:
+            dk = dev(np.concatenate([np.zeros(off, np.uint32), keys[lo:hi]]))[off:]
+            dv = dev(np.concatenate([np.zeros(off, np.uint32), vals[lo:hi]]))[off:]
+            if how == "chunked":
+                table.build_feed(dk, dv)
+                continue
+            o = table.insert(dk, dv)
         inserted += o.inserted
         failed += o.failed
-    desc = f"kind={kind} b={b} lf={lf} n={n} mode={mode} batches={cuts} throttle={throttle} off={off}"
+    if how == "chunked":
+        o = table.build_end()
+        inserted, failed = o.inserted, o.failed
+    desc = f"kind={kind} b={b} lf={lf} n={n} mode={mode} batches={cuts} throttle={throttle} off={off} how={how}"
     assert inserted + failed == n, desc
     assert table.occupied_slots() == inserted and table.count_inadmissible() == 0, desc
     store = table.download_store()
