@@ -228,3 +228,40 @@ def test_build_success_at_load_099_matches_the_reference(bht, ref):
     # one pair per launch is insert_pair exactly: a failing insertion is not given a second chain (scenario tests pin
     # the probe counts); 1cht keeps the raw outcome by default
     assert bht.HashTable(bht.make_config("1cht", 1000, 0.5, 1, seed=1), 0) is not None
+
+
+@pytest.mark.parametrize("b,lf", [(1, 0.8), (2, 0.85), (4, 0.9), (8, 0.9), (16, 0.9)])
+def test_blocked_build_probe_shift_by_bucket_size(bht, ora, b, lf):
+    """The shared-memory-blocked build makes every first attempt before any eviction walk; the reference interleaves
+    them.  At b = 1 that shifts the insert probe mean 1.6-3 % below the reference's (which is why 1cht keeps the
+    L2-routed schedule by default); this pins where the shift stops mattering (measured, insert / find-100 means against the
+    oracle's sequential build: b = 1 3.2 %, b = 2 2.2 %, b = 4 1.0 %, b = 8 0.2 %, b = 16 0.15 %; the general kernel in
+    caller order is itself 1.2-2 % off at b = 1, 2)."""
+    n = 1_000_000
+    keys = unique_keys(n, 600 + b, extra=n)
+    present, absent = keys[:n], keys[n:]
+    kind = "1cht" if b == 1 else "bcht"
+    cfg = bht.make_config(kind, n, lf, b, seed=bht.mix_seed(41, b))
+    otab = ora.table(to_oracle_cfg(cfg))
+    r = otab.insert_all(present)
+    assert r["inserted"] == n
+    ref_ins = r["probes"] / n
+    _, _, p_pos = otab.find_bulk(present)
+    _, _, p_neg = otab.find_bulk(absent)
+    got = {}
+    for mode in (0, 3):
+        t = bht.HashTable(cfg, 0)
+        t.set_blocked_insert(mode)
+        o = t.insert(dev(present))
+        assert o.success and t.last_build_schedule() == mode
+        _, sp = t.find(dev(present), want_stats=True)
+        _, sn = t.find(dev(absent), want_stats=True)
+        got[mode] = (o.mean_probes, sp.mean_probes, sn.mean_probes)
+        t.close()
+    ref = (ref_ins, p_pos / n, p_neg / n)
+    shift = [abs(g - w) / w for g, w in zip(got[3], ref)]
+    base = [abs(g - w) / w for g, w in zip(got[0], ref)]
+    print(f"b={b} lf={lf}: reference {ref}, caller order {got[0]}, blocked {got[3]}; shift {shift}")
+    assert max(base) < 0.02  # the general kernel follows the reference's process at every bucket size
+    tol = {1: 0.045, 2: 0.035, 4: 0.015, 8: 0.006, 16: 0.004}[b]
+    assert max(shift) < tol, (b, shift)
