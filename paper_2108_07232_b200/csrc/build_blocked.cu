@@ -41,6 +41,7 @@
 // of the walk.  A pair that overflows a bin or the stash reaches K4 untouched and is counted there from H0 on.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 
 #include "insert_common.cuh"
@@ -463,7 +464,6 @@ region_build_kernel(const __grid_constant__ TableView t, uint32_t region_log2, u
   uint32_t* cnt = reinterpret_cast<uint32_t*>(sm_bytes + (static_cast<size_t>(region_buckets) << (b_log2 + 3)));
   uint16_t* stash = reinterpret_cast<uint16_t*>(cnt + region_buckets);  // positions (in the bin) of the pairs whose bucket was full
   __shared__ uint32_t stash_count, hole_count;
-  __shared__ unsigned long long stash_base;
   const uint32_t region = blockIdx.x;
   const uint64_t first = static_cast<uint64_t>(region) << region_log2;
   const uint32_t first32 = static_cast<uint32_t>(first);
@@ -479,6 +479,31 @@ region_build_kernel(const __grid_constant__ TableView t, uint32_t region_log2, u
     const char* base = reinterpret_cast<const char*>(bins + static_cast<uint64_t>(r2) * cap);
     for (uint32_t off = threadIdx.x * 128u; off < bytes; off += kBuildBlock * 128u) prefetch_l2(base + off);
   }
+
+#ifdef BHT_K11_TIMING
+  long long tk[8];
+  tk[0] = clock64();
+#define TK(i) tk[i] = clock64()
+#else
+#define TK(i)
+#endif
+  // The bin's pairs arrive two per 16-byte load, U loads per thread and batch; the loads of batch k + 1 are in flight
+  // while batch k is processed, and those of the first batch while the region is set up (phase 0).
+  const uint32_t n_r = min(bin_cursor[region], cap);
+  const uint2* bin = bins + static_cast<uint64_t>(region) * cap;  // 16-byte aligned: cap is even
+  const uint4* bin4 = reinterpret_cast<const uint4*>(bin);
+  const uint32_t n_units = (n_r + 1u) >> 1;
+  constexpr int U = BHT_BUILD_U / 2;
+  uint4 v_next[U];
+  auto load_batch = [&](uint32_t q0) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t q = q0 + u * kBuildBlock;
+      v_next[u] = make_uint4(0u, 0u, 0u, 0u);
+      if (q < n_units) v_next[u] = __ldcs(bin4 + q);  // an odd bin's last unit reads one pair of slack inside the bin's capacity
+    }
+  };
+  load_batch(threadIdx.x);
 
   // phase 0: the region's buckets into shared memory
   {
@@ -507,31 +532,21 @@ region_build_kernel(const __grid_constant__ TableView t, uint32_t region_log2, u
     __syncthreads();
   }
 
+  TK(1);
   // phase 1: every pair of the bin claims slot = load++ of its bucket (a shared-memory atomic: no CAS, no lost race).
-  // Two pairs per 16-byte load, BHT_BUILD_U pairs in flight per thread.  A pair whose bucket is full only leaves a bit
-  // in `spilled`; after the unrolled block the thread notes the bin positions of those pairs in the CTA's stash.
-  const uint32_t n_r = min(bin_cursor[region], cap);
-  const uint2* bin = bins + static_cast<uint64_t>(region) * cap;  // 16-byte aligned: cap is even
-  const uint4* bin4 = reinterpret_cast<const uint4*>(bin);
-  const uint32_t n_units = (n_r + 1u) >> 1;
-  constexpr int U = BHT_BUILD_U / 2;
+  // A pair whose bucket is full only leaves a bit in `spilled`; after the unrolled block the thread notes the bin
+  // positions of those pairs in the CTA's stash.
   for (uint32_t q0 = threadIdx.x; q0 < n_units; q0 += kBuildBlock * U) {
+    uint4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = v_next[u];
+    if (q0 + kBuildBlock * U < n_units) load_batch(q0 + kBuildBlock * U);
     uint32_t spilled = 0;
     if (2u * (q0 + (U - 1) * kBuildBlock) + 1u < n_r) {  // every pair of the thread's U units exists: no predicates
-      uint4 v[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) v[u] = __ldcs(bin4 + q0 + u * kBuildBlock);
 #pragma unroll
       for (int u = 0; u < U; ++u)
         spilled |= claim_unit<false>(v[u], q0 + u * kBuildBlock, n_r, t.h[0], first32, nb, b_log2, B, rows, cnt) << (2 * u);
     } else {
-      uint4 v[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const uint32_t q = q0 + u * kBuildBlock;
-        v[u] = make_uint4(0u, 0u, 0u, 0u);
-        if (q < n_units) v[u] = __ldcs(bin4 + q);  // an odd bin's last unit reads one pair of slack inside the bin's capacity
-      }
 #pragma unroll
       for (int u = 0; u < U; ++u)
         spilled |= claim_unit<true>(v[u], q0 + u * kBuildBlock, n_r, t.h[0], first32, nb, b_log2, B, rows, cnt) << (2 * u);
@@ -545,47 +560,70 @@ region_build_kernel(const __grid_constant__ TableView t, uint32_t region_log2, u
       else spill_fresh(bin[idx], sp);  // past the stash: straight to the list, untouched
     }
   }
+  TK(2);
   __syncthreads();  // every claimed slot is written
+  TK(3);
 
   // phase 1b: the first eviction of the stashed pairs, in shared memory (table.cpp:67-81): the pair goes into a random
   // slot of its full bucket, the victim goes to the spill list with the bucket named by the hash function after the
   // lowest-index one that maps it here, and a chain length of 1.  One probe (the inspection that found the bucket full).
+  // Every warp reserves the list entries of its 32 stashed pairs itself, and first: the reservation (a global atomic)
+  // and the re-read of the pairs from the bin travel while the warp does the evictions.
   const uint32_t spilled_total = stash_count;
   const uint32_t stashed = min(spilled_total, kStashPairs);
-  if (threadIdx.x == 0 && stashed != 0) stash_base = atomicAdd(sp.cursor, static_cast<unsigned long long>(stashed));
-  __syncthreads();
   if (stashed != 0) {
+    const int lane = threadIdx.x & 31;
     uint64_t rng = xorshift_init(mix_seed(t.seed, 0x626C6B64ull + static_cast<uint64_t>(blockIdx.x) * kBuildBlock + threadIdx.x));
-    for (uint32_t i = threadIdx.x; i < stashed; i += kBuildBlock) {
-      const uint2 p = bin[stash[i]];
-      const uint32_t bid = bucket_index(t.h[0], p.x);
-      const uint32_t lb = bid - first32;
-      const unsigned long long old = atomicExch(rows + (lb << b_log2) + xorshift_next_below(rng, B), pack_pair(p.x, p.y));
-      const uint32_t vk = static_cast<uint32_t>(old);
-      uint32_t next = 0;
-      if (vk != kEmptyKey) {
-        uint32_t cand[4];
+    for (uint32_t i0 = threadIdx.x - lane; i0 < stashed; i0 += kBuildBlock) {  // warp-uniform
+      const uint32_t i = i0 + lane;
+      const bool mine = i < stashed;
+      unsigned long long base = 0;
+      if (lane == 0) base = atomicAdd(sp.cursor, static_cast<unsigned long long>(min(32u, stashed - i0)));
+      uint2 p = make_uint2(0u, 0u);
+      if (mine) p = bin[stash[i]];
+      uint32_t vk = kEmptyKey, vv = 0, next = 0;
+      if (mine) {
+        const uint32_t bid = bucket_index(t.h[0], p.x);
+        const uint32_t lb = bid - first32;
+        const unsigned long long old = atomicExch(rows + (lb << b_log2) + xorshift_next_below(rng, B), pack_pair(p.x, p.y));
+        vk = static_cast<uint32_t>(old);
+        vv = static_cast<uint32_t>(old >> 32);
+        if (vk != kEmptyKey) {
+          if (fresh) {
+            // every pair of a freshly built region sits in its H0 bucket, so the lowest-index hash function that maps
+            // the victim here is H0 and its walk goes on at H1 (table.cpp:74-80)
+            next = bucket_index(t.h[1], vk);
+          } else {
+            uint32_t cand[4];
 #pragma unroll
-        for (int h = 0; h < 4; ++h) cand[h] = h < static_cast<int>(t.n_hashes) ? bucket_index(t.h[h], vk) : 0u;
-        next = cand[0];
+            for (int h = 0; h < 4; ++h) cand[h] = h < static_cast<int>(t.n_hashes) ? bucket_index(t.h[h], vk) : 0u;
+            next = cand[0];
 #pragma unroll
-        for (int h = 3; h >= 0; --h)  // lowest matching index wins (table.cpp:74-80)
-          if (h < static_cast<int>(t.n_hashes) && cand[h] == bid) next = cand[h + 1 < static_cast<int>(t.n_hashes) ? h + 1 : 0];
+            for (int h = 3; h >= 0; --h)  // lowest matching index wins (table.cpp:74-80)
+              if (h < static_cast<int>(t.n_hashes) && cand[h] == bid) next = cand[h + 1 < static_cast<int>(t.n_hashes) ? h + 1 : 0];
+          }
+        } else {
+          atomicAdd(&hole_count, 1u);  // a hole (only on an uploaded store): the pair is simply placed; the list entry becomes a tombstone
+        }
       }
-      // a hole (only on an uploaded store): the pair is simply placed; the reserved list entry becomes a tombstone
-      if (vk == kEmptyKey) atomicAdd(&hole_count, 1u);
-      if (stash_base + i < sp.cap) {
-        sp.pairs[stash_base + i] = make_uint2(vk, static_cast<uint32_t>(old >> 32));
-        sp.start[stash_base + i] = vk == kEmptyKey ? kStartTombstone : (next | 0x80000000u);
-      } else if (vk != kEmptyKey) {
-        spill_dropped(vk, sp);  // the victim in hand is the pair dropped, as when a chain hits its cap
+      base = __shfl_sync(kFullMask, base, 0);
+      if (mine) {
+        const unsigned long long at = base + lane;
+        if (at < sp.cap) {
+          sp.pairs[at] = make_uint2(vk, vv);
+          sp.start[at] = vk == kEmptyKey ? kStartTombstone : (next | 0x80000000u);
+        } else if (vk != kEmptyKey) {
+          spill_dropped(vk, sp);  // the victim in hand is the pair dropped, as when a chain hits its cap
+        }
       }
     }
   }
+  TK(4);
 #if BHT_BUILD_TMA_STORE
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // this thread's shared-memory writes, for the bulk-copy engine
 #endif
   __syncthreads();
+  TK(5);
 
   // phase 2: the region back to the store
   {
@@ -622,6 +660,12 @@ region_build_kernel(const __grid_constant__ TableView t, uint32_t region_log2, u
     asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // shared memory may go once the copies have read it
 #endif
   }
+#ifdef BHT_K11_TIMING
+  TK(6);
+  if ((blockIdx.x % 997) == 5 && (threadIdx.x == 0 || threadIdx.x == 200))
+    printf("K11 cta %u thr %u: fill %lld  claim-loop %lld  wait-claims %lld  evict %lld  wait-evict %lld  writeback %lld  total %lld (n_r %u stashed %u)\n",
+           blockIdx.x, threadIdx.x, tk[1] - tk[0], tk[2] - tk[1], tk[3] - tk[2], tk[4] - tk[3], tk[5] - tk[4], tk[6] - tk[5], tk[6] - tk[0], n_r, stashed);
+#endif
 }
 
 }  // namespace
