@@ -624,6 +624,9 @@ def run_cuda(args):
     cpu = None
     if rank == 0 and not args.no_cpu_baseline and n <= 100_000_000:
         cpu = cpu_baseline_leg(args, keys.cpu().numpy().view(np.uint32), n)
+    barrier()  # the other ranks wait for rank 0's CPU leg before the group is torn down
+    if world == 1:
+        wl["parallelism"] = "the sharded path with a world of one (no routing: one shard owns every key)"
     if rank == 0:
         value = 2 * n * world / (ms_step * 1e-3) / 1e6
         peaks = load_peaks()
