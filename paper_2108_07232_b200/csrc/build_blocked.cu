@@ -315,12 +315,7 @@ group_scatter_kernel(const __grid_constant__ GroupArgs args) {
     for (int j = 0; j < kSplitPerThread; ++j) {
       const uint32_t d = group_of(kv[j].x);
       uint32_t rank = 0;
-#if defined(BHT_EXP_NOATOMS)  // experiment (wrong results): the pass without its shared-memory ranking
-      rank = (threadIdx.x * 8 + j) & 15u;
-      if (threadIdx.x < 83 && j == 0) s.hist[threadIdx.x] = 24;
-#else
       if ((valid >> j) & 1u) rank = atomicAdd(&s.hist[d], 1u);
-#endif
       dr[j] = d | (rank << 8);
     }
     __syncthreads();  // every rank of the tile is taken, and `in` has been read by everyone
@@ -442,7 +437,7 @@ __device__ __forceinline__ uint32_t claim_unit(const uint4 v, uint32_t q, uint32
     const uint32_t k = e ? v.z : v.x, val = e ? v.w : v.y;
     if (!GUARD || 2u * q + e < n_r) {
       const uint32_t lb = bucket_index(h0, k) - first32;  // < nb: the bin holds pairs of this region only
-#if defined(BHT_EXP_NOSTORE) || defined(BHT_EXP_LINEAR) || defined(BHT_EXP_NOGATOM) || defined(BHT_EXP_NOATOMS)
+#if defined(BHT_EXP_NOSTORE) || defined(BHT_EXP_LINEAR) || defined(BHT_EXP_NOGATOM)
       if (lb >= nb) continue;  // the experiments feed this kernel garbage
 #endif
       const uint32_t slot = atomicAdd(&cnt[lb], 1u);
