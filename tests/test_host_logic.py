@@ -207,3 +207,44 @@ def test_shard_constants_same_in_c_and_python(bht):
         lib.bht_shard_constants(seed, C.byref(a), C.byref(b))
         assert (a.value, b.value) == tuple(bht.shard_constants(seed))
         assert 1 <= a.value < 4294967291 and b.value < 4294967291
+
+
+def test_bench_reference_arm_contract(ref):
+    """`bench.py --impl reference` (the arm the driver runs beside the CUDA one): ONE JSON line on stdout with the
+    contract's keys, the reference's own CPU path timed on this host's cores, no GPU needed.  A small key count keeps
+    it to seconds; --config names any BASELINE.json cell."""
+    import json
+    import subprocess
+    import sys
+    for extra in ([], ["--config", "bp2ht08"]):
+        r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "1", "--warmup", "0",
+                            "--keys", "300000", "--workload", "numpy"] + extra, capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        lines = [ln for ln in r.stdout.splitlines() if ln.strip()]
+        assert len(lines) == 1, r.stdout
+        line = json.loads(lines[0])
+        for key in ("impl", "metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+                    "vs_baseline", "dtype", "data", "config", "cpu_baseline", "e2e"):
+            assert key in line, key
+        assert line["impl"] == "reference" and line["unit"] == "MKeys/s" and line["value"] > 0
+        assert line["cpu_baseline"]["kind"] == "reference" and line["cpu_baseline"]["cores"] >= 1
+        assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["value"] == line["value"]
+        if extra:
+            assert "BP2HT" in line["metric"] and line["config"]["kind"] == "bp2ht"
+
+
+def test_bench_configs_cover_baseline_json():
+    """Every configuration BASELINE.json names is a `--config` of bench.py."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(ROOT, "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    cells = set(bench.CONFIGS.values())
+    for want in [("bcht", 16, 0.8, None), ("bcht", 16, 0.9, None), ("bcht", 16, 0.99, None), ("1cht", 1, 0.8, None),
+                 ("1cht", 1, 0.9, None), ("bp2ht", 16, 0.6, None), ("bp2ht", 16, 0.99, None), ("iht", 16, 0.9, 12),
+                 ("iht", 16, 0.99, 12)]:
+        assert want in cells, want
+    bench.select_config("iht:32:0.9:25")
+    assert (bench.KIND, bench.B, bench.LF, bench.THRESHOLD) == ("iht", 32, 0.9, 25) and "IHT b=32, t=25" in bench.METRIC
+    bench.select_config("headline")
+    assert bench.METRIC == "insert & find MKeys/s, BCHT b=16, 50M keys, LF 0.9" and bench.HEADLINE
