@@ -470,6 +470,15 @@ def run_cuda(args):
         roofline["frac_of_8TBps"] = dom_bytes / (dom_ms * 1e-3) / 8e12
         # the stricter variant: the sector model plus the streamed arrays (find: 4 B key in + 4 B value out; insert: 8 B in)
         roofline["frac_with_streaming_io"] = (dom_bytes + 8 * n) / (dom_ms * 1e-3) / 1e9 / peaks["hbm_gbs"]
+        # the other ceiling of this part: HBM serves ~48.7 G random accesses per second whatever their size up to 128 B
+        # (tools/microbench, profiles/r01_microbench_gather_atomics.txt: 128-byte line gathers over 444 MB).  b = 16 is the
+        # bucket size at which that rate equals the byte roof; smaller buckets (b = 8: 64 B, 1cht: 8 B) hit the access
+        # rate at a fraction of the bytes, which is what their `frac` below 1 means.
+        rate_peak = 48.7e9
+        dom_probes = (outcome.mean_probes + 1.0 if dom_insert else fs100.mean_probes) * n  # an insert also writes a dirtied sector back
+        roofline["access_rate"] = {"bound": "hbm random accesses", "achieved": dom_probes / (dom_ms * 1e-3) / 1e9, "peak": rate_peak / 1e9,
+                                   "unit": "G accesses/s", "frac": dom_probes / (dom_ms * 1e-3) / rate_peak,
+                                   "peak_source": "profiles/r01_microbench_gather_atomics.txt (random 128 B line gather, 444 MB)"}
         roofline["note"] = ("achieved = sector-model bytes (probes x 4 sectors, + 1 written sector per inserted pair, x 32 B) / "
                             "this kernel's CUDA-event time; traffic = its ncu dram bytes per launch (L2 hits make it smaller "
                             "than the model). detail.roofline_insert_op is the whole bulk insert (partition passes, "
