@@ -280,6 +280,7 @@ bht_status bht_shard_partition(uint64_t alpha, uint64_t beta, uint32_t n_shards,
 /* bht_shard_partition without any host synchronisation, for an all-to-all with EQUAL splits: destination d gets the
  * slots [d * cap, (d + 1) * cap) of the outputs (the caller pre-fills them with 0xFF bytes: unused slots then hold the
  * sentinel key / the index 0xFFFFFFFF, which bht_find answers without a probe and bht_shard_unpermute skips);
+ * An element carries its value (values != NULL, inserts) or its position in the input (out_index != NULL, finds), not both.
  * counts_dev[d] (device, uint64) = elements written for d; *overflow_dev (device) is OR-ed with 1 when some destination
  * had more than cap elements (the surplus is not written: the caller re-routes with exact counts). */
 bht_status bht_shard_partition_fixed(uint64_t alpha, uint64_t beta, uint32_t n_shards, const uint32_t* keys,

@@ -1364,14 +1364,16 @@ bht_status bht_shard_partition_fixed(uint64_t alpha, uint64_t beta, uint32_t n_s
   if (counts_dev == nullptr || overflow_dev == nullptr || (n != 0 && (keys == nullptr || out_keys == nullptr)) ||
       (values != nullptr && out_values == nullptr))
     return fail(BHT_INVALID_ARGUMENT, "bht_shard_partition_fixed: null argument");
+  if (values != nullptr && out_index != nullptr)
+    return fail(BHT_INVALID_ARGUMENT, "bht_shard_partition_fixed: an element carries its value (inserts) or its position (finds), not both");
   BHT_ON_DEVICE(device);
   const int sm_count = device_sm_count(device);
   cudaStream_t s = as_stream(stream);
-  unsigned long long* scratch = nullptr;  // cursors | n destination bytes
-  BHT_CUDA(cudaMallocAsync(&scratch, sizeof(unsigned long long) * n_shards + n + 16, s));
-  const cudaError_t e = launch_shard_route_fixed(static_cast<uint32_t>(alpha), static_cast<uint32_t>(beta), n_shards, keys, values, n, cap,
-                                                 reinterpret_cast<uint8_t*>(scratch + n_shards),
-                                                 reinterpret_cast<unsigned long long*>(counts_dev), scratch, overflow_dev, out_keys,
+  uint32_t* scratch = nullptr;  // one cursor word per destination
+  BHT_CUDA(cudaMallocAsync(&scratch, sizeof(uint32_t) * n_shards, s));
+  // index mode without values: the second output array carries the positions; a keys-only call carries nothing
+  const cudaError_t e = launch_shard_split_fixed(static_cast<uint32_t>(alpha), static_cast<uint32_t>(beta), n_shards, keys, values, n, cap,
+                                                 scratch, reinterpret_cast<unsigned long long*>(counts_dev), overflow_dev, out_keys,
                                                  out_values, out_index, sm_count, s);
   cudaFreeAsync(scratch, s);
   if (e != cudaSuccess) return cuda_fail(e, "bht_shard_partition_fixed");

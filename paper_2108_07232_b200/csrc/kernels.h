@@ -103,12 +103,13 @@ constexpr int kMaxShards = 256;
 cudaError_t launch_shard_route(uint32_t alpha, uint32_t beta, uint32_t n_shards, const uint32_t* keys, const uint32_t* values,
                                uint64_t n, uint8_t* scratch8, unsigned long long* counts, unsigned long long* cursors,
                                uint32_t* out_keys, uint32_t* out_values, uint32_t* out_index, int sm_count, cudaStream_t stream);
-// The same routing into fixed segments of `cap` elements per destination (what a sync-free all-to-all with equal splits
-// sends): counts (device) are clamped to cap, *overflow is set when a destination had more.  Nothing is copied to the host.
-cudaError_t launch_shard_route_fixed(uint32_t alpha, uint32_t beta, uint32_t n_shards, const uint32_t* keys, const uint32_t* values,
-                                     uint64_t n, uint64_t cap, uint8_t* scratch8, unsigned long long* counts,
-                                     unsigned long long* cursors, uint32_t* overflow, uint32_t* out_keys, uint32_t* out_values,
-                                     uint32_t* out_index, int sm_count, cudaStream_t stream);
+// K8s (build_blocked.cu): routing into fixed segments of `cap` elements per destination (what a sync-free all-to-all with
+// equal splits sends) in ONE pass with the partition machinery of the blocked build (no classify pass, no destination
+// bytes).  counts (device) are clamped to cap, *overflow is set when a destination had more; nothing is copied to the
+// host.  insert side: values != null; find side: out_index receives the elements' positions.
+cudaError_t launch_shard_split_fixed(uint32_t alpha, uint32_t beta, uint32_t n_shards, const uint32_t* keys, const uint32_t* values,
+                                     uint64_t n, uint64_t cap, uint32_t* cursor32, unsigned long long* counts, uint32_t* overflow,
+                                     uint32_t* out_keys, uint32_t* out_values, uint32_t* out_index, int sm_count, cudaStream_t stream);
 // Groups pairs by the table region (n_regions contiguous ranges of buckets) of their first bucket; out_pairs
 // receives n packed {key, value} pairs (8 bytes each).
 cudaError_t launch_region_route(const HashFn& h0, uint32_t n_regions, const uint32_t* keys, const uint32_t* values, uint64_t n,

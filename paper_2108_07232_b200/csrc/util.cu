@@ -243,8 +243,7 @@ template <bool PACKED, bool INDEX>
 __global__ void __launch_bounds__(kStreamBlock)
 route_scatter_kernel(uint32_t n_dest, const uint32_t* __restrict__ keys, const uint32_t* __restrict__ values,
                      const uint8_t* __restrict__ dest8, uint64_t n, bool aligned, unsigned long long* __restrict__ cursors,
-                     uint32_t* __restrict__ out_keys, uint32_t* __restrict__ out_values, uint32_t* __restrict__ out_index,
-                     const uint64_t seg_cap) {  // != 0: destination d owns [d * seg_cap, (d + 1) * seg_cap) and nothing is written past it
+                     uint32_t* __restrict__ out_keys, uint32_t* __restrict__ out_values, uint32_t* __restrict__ out_index) {
   __shared__ uint2 s_pair[kTile];       // {key, value} grouped by destination
   __shared__ uint8_t s_dest[kTile];
   __shared__ uint32_t s_index[INDEX ? kTile : 1];
@@ -326,7 +325,6 @@ route_scatter_kernel(uint32_t n_dest, const uint32_t* __restrict__ keys, const u
         const uint32_t d = s_dest[slot];
         const unsigned long long pos = base_of[d] + (slot - tile_off[d]);
         const uint2 kv = s_pair[slot];
-        if (seg_cap != 0 && pos >= (static_cast<unsigned long long>(d) + 1) * seg_cap) continue;  // the caller sees the overflow flag
         if constexpr (PACKED) {
           __stcs(reinterpret_cast<uint2*>(out_keys) + pos, kv);
         } else {
@@ -363,53 +361,7 @@ static cudaError_t route(const Router& r, uint32_t n_dest, const uint32_t* keys,
   note_launch();
   if (n != 0) {
     route_scatter_kernel<PACKED, INDEX><<<stream_grid(sm_count, n, kTile, 8), kStreamBlock, 0, stream>>>(
-        n_dest, keys, values, scratch8, n, aligned, cursors, out_keys, out_values, out_index, 0);
-    note_launch();
-  }
-  return cudaGetLastError();
-}
-
-// Fixed segments: destination d gets slots [d * cap, (d + 1) * cap) of the outputs, whatever the counts.  counts[d] is
-// clamped to cap and *overflow is raised when a destination had more (its surplus elements are NOT written).
-__global__ void route_fixed_cursors_kernel(uint32_t n_dest, uint64_t cap, unsigned long long* __restrict__ counts,
-                                           unsigned long long* __restrict__ cursors, uint32_t* __restrict__ overflow) {
-  const uint32_t d = blockIdx.x * blockDim.x + threadIdx.x;
-  if (d >= n_dest) return;
-  cursors[d] = static_cast<unsigned long long>(d) * cap;
-  if (counts[d] > cap) {
-    counts[d] = cap;
-    atomicOr(overflow, 1u);
-  }
-}
-
-cudaError_t launch_shard_route_fixed(uint32_t alpha, uint32_t beta, uint32_t n_shards, const uint32_t* keys, const uint32_t* values,
-                                     uint64_t n, uint64_t cap, uint8_t* scratch8, unsigned long long* counts,
-                                     unsigned long long* cursors, uint32_t* overflow, uint32_t* out_keys, uint32_t* out_values,
-                                     uint32_t* out_index, int sm_count, cudaStream_t stream) {
-  if (n_shards == 0 || n_shards > static_cast<uint32_t>(kMaxShards)) return cudaErrorInvalidValue;
-  const ShardRouter r{alpha, beta, n_shards};
-  cudaError_t e = cudaMemsetAsync(counts, 0, sizeof(unsigned long long) * n_shards, stream);
-  if (e != cudaSuccess) return e;
-  const bool aligned = ((reinterpret_cast<uintptr_t>(keys) | reinterpret_cast<uintptr_t>(values)) & 15) == 0;
-  if (n != 0) {
-    const bool priv = n_shards <= 48;
-    auto kernel = priv ? route_classify_kernel<ShardRouter, true> : route_classify_kernel<ShardRouter, false>;
-    const int smem = static_cast<int>(n_shards * (priv ? kStreamBlock : 1) * sizeof(uint32_t));
-    int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kStreamBlock, smem) != cudaSuccess || per_sm < 1) per_sm = 1;
-    kernel<<<stream_grid(sm_count, n, kStreamBlock * 16, per_sm), kStreamBlock, smem, stream>>>(r, n_shards, keys, n, aligned, scratch8,
-                                                                                              counts);
-    note_launch();
-  }
-  route_fixed_cursors_kernel<<<(n_shards + 255) / 256, 256, 0, stream>>>(n_shards, cap, counts, cursors, overflow);
-  note_launch();
-  if (n != 0) {
-    if (out_index != nullptr)
-      route_scatter_kernel<false, true><<<stream_grid(sm_count, n, kTile, 8), kStreamBlock, 0, stream>>>(
-          n_shards, keys, values, scratch8, n, aligned, cursors, out_keys, out_values, out_index, cap);
-    else
-      route_scatter_kernel<false, false><<<stream_grid(sm_count, n, kTile, 8), kStreamBlock, 0, stream>>>(
-          n_shards, keys, values, scratch8, n, aligned, cursors, out_keys, out_values, nullptr, cap);
+        n_dest, keys, values, scratch8, n, aligned, cursors, out_keys, out_values, out_index);
     note_launch();
   }
   return cudaGetLastError();

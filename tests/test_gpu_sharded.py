@@ -92,26 +92,35 @@ def test_fixed_segment_partition_against_numpy(bht):
     alpha, beta = bht.shard_constants(cfg.seed)
     lib = bht._lib.load()
     owner = np.array([lib.bht_shard_of_host(alpha, beta, world, int(k)) for k in keys[:20000]])
-    cap = int(n / world * 1.05)
-    sk, sv, idx, counts = ops.partition_fixed(alpha, beta, world, d(keys), d(vals), True, cap)
+    cap = int(n / world * 1.05) & ~3
+    # an element carries its value (inserts) or its position (finds): one call each
+    sk, sv, _, counts = ops.partition_fixed(alpha, beta, world, d(keys), d(vals), False, cap)
+    sk2, _, idx, counts2 = ops.partition_fixed(alpha, beta, world, d(keys), None, True, cap)
     torch.cuda.synchronize()
     assert int(ops.overflow.item()) == 0
-    sk, sv, idx, counts = (x.cpu().numpy() for x in (sk, sv, idx, counts))
-    assert counts.sum() == n
+    sk, sv, counts, sk2, idx, counts2 = (x.cpu().numpy() for x in (sk, sv, counts, sk2, idx, counts2))
+    assert counts.sum() == n and np.array_equal(counts, counts2)
+    lookup = dict(zip(keys.tolist(), vals.tolist()))
     for g in range(world):
-        seg_k = sk[g * cap:(g + 1) * cap].view(np.uint32)
-        seg_i = idx[g * cap:(g + 1) * cap].view(np.uint32)
         c = int(counts[g])
-        assert np.all(seg_k[c:] == EMPTY) and np.all(seg_i[c:] == EMPTY)  # padding: sentinel key, no index
-        assert np.array_equal(keys[seg_i[:c]], seg_k[:c])
-        assert np.array_equal(vals[seg_i[:c]], sv[g * cap:g * cap + c].view(np.uint32))
+        seg_k = sk[g * cap:(g + 1) * cap].view(np.uint32)
+        seg_v = sv[g * cap:g * cap + c].view(np.uint32)
+        assert np.all(seg_k[c:] == EMPTY)  # padding: the sentinel key
+        assert np.array_equal(np.array([lookup[int(k)] for k in seg_k[:3000]], dtype=np.uint32), seg_v[:3000])  # pairs stay pairs
+        seg_k2 = sk2[g * cap:(g + 1) * cap].view(np.uint32)
+        seg_i = idx[g * cap:(g + 1) * cap].view(np.uint32)
+        assert np.all(seg_k2[c:] == EMPTY) and np.all(seg_i[c:] == EMPTY)  # padding: sentinel key, no index
+        assert np.array_equal(keys[seg_i[:c]], seg_k2[:c])  # the index names the element's position in the input
+        assert np.array_equal(np.sort(seg_k2[:c]), np.sort(seg_k[:c]))  # both calls route the same keys to g
         small = seg_i[:c][seg_i[:c] < 20000]
         assert np.all(owner[small] == g)
+    with pytest.raises(ValueError):
+        ops.partition_fixed(alpha, beta, world, d(keys), d(vals), True, cap)  # not both
     # a segment that is too small: flagged, counts clamped, neighbours' segments intact
     cap2 = int(n / world * 0.9) & ~3
-    sk2, _, _, counts2 = ops.partition_fixed(alpha, beta, world, d(keys), None, False, cap2)
+    sk3, _, _, counts3 = ops.partition_fixed(alpha, beta, world, d(keys), None, False, cap2)
     torch.cuda.synchronize()
-    assert int(ops.overflow.item()) == 1 and int(counts2.max().item()) == cap2
-    sk2 = sk2.cpu().numpy().view(np.uint32)
-    own2 = np.array([lib.bht_shard_of_host(alpha, beta, world, int(k)) for k in sk2[cap2:cap2 + 3000]])
-    assert np.all(own2 == 1)
+    assert int(ops.overflow.item()) == 1 and int(counts3.max().item()) == cap2
+    sk3 = sk3.cpu().numpy().view(np.uint32)
+    own3 = np.array([lib.bht_shard_of_host(alpha, beta, world, int(k)) for k in sk3[cap2:cap2 + 3000]])
+    assert np.all(own3 == 1)
