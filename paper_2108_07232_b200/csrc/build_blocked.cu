@@ -21,7 +21,7 @@
 //                       lost races, no re-probes — and the region is written back by the bulk-copy engine
 //                       (cp.async.bulk shared -> global, SASS UBLKCP, 4 KiB pieces: 0.771 -> 0.746 ms for the three
 //                       passes against coalesced 16-byte stores from registers).
-//                       A pair whose bucket is full leaves its bin position in a per-CTA stash; once every claim is
+//                       A pair whose bucket is full goes to a per-CTA stash in shared memory; once every claim is
 //                       written the stashed pairs do their first eviction in shared memory (atomicExch into a random
 //                       slot of the full bucket, table.cpp:67-81) and the VICTIMS go to the global spill list, each
 //                       with the bucket its walk goes on in and a chain length of 1 (one list reservation per CTA).
@@ -77,7 +77,7 @@ constexpr int kSplitBlock = BHT_SPLIT_BLOCK;  // >= 256: the first 256 threads s
 constexpr int kSplitPerThread = 8;
 constexpr int kSplitTile = kSplitBlock * kSplitPerThread;  // 2048 pairs
 constexpr int kBuildBlock = BHT_BUILD_BLOCK;   // few threads with many loads in flight each: 3 CTAs/SM by shared memory
-constexpr uint32_t kStashPairs = 4096;  // per-CTA stash of spilled pairs (K11): 16-bit positions in the region's bin
+constexpr uint32_t kStashPairs = 1024;  // per-CTA stash of the pairs whose bucket was full (K11): 8 KiB beside the region's 64
 constexpr uint32_t kRegionBytesLog2 = 16;
 
 // The spill list: packed pairs + where their walk starts (kStartAtH0 for a pair that has not probed anything yet).
@@ -580,7 +580,7 @@ __device__ __forceinline__ uint32_t claim_unit(const uint4 v, uint32_t q, uint32
   return spilled;
 }
 
-__global__ void __launch_bounds__(kBuildBlock)
+__global__ void __launch_bounds__(kBuildBlock, 3)
 region_build_kernel(const __grid_constant__ TableView t, uint32_t region_log2, uint32_t b_log2, uint32_t cap,
                     const uint32_t* __restrict__ bin_cursor, const uint2* __restrict__ bins, int fresh, const Spill sp,
                     DevCounters* __restrict__ ctr, uint32_t ahead) {
@@ -589,7 +589,7 @@ region_build_kernel(const __grid_constant__ TableView t, uint32_t region_log2, u
   const uint32_t B = 1u << b_log2;
   unsigned long long* rows = reinterpret_cast<unsigned long long*>(sm_bytes);  // region_buckets * B slots
   uint32_t* cnt = reinterpret_cast<uint32_t*>(sm_bytes + (static_cast<size_t>(region_buckets) << (b_log2 + 3)));
-  uint16_t* stash = reinterpret_cast<uint16_t*>(cnt + region_buckets);  // positions (in the bin) of the pairs whose bucket was full
+  uint2* stash = reinterpret_cast<uint2*>(cnt + region_buckets);  // the pairs whose bucket was full
   __shared__ uint32_t stash_count, hole_count;
   const uint32_t region = blockIdx.x;
   const uint64_t first = static_cast<uint64_t>(region) << region_log2;
@@ -661,8 +661,8 @@ region_build_kernel(const __grid_constant__ TableView t, uint32_t region_log2, u
 
   TK(1);
   // phase 1: every pair of the bin claims slot = load++ of its bucket (a shared-memory atomic: no CAS, no lost race).
-  // A pair whose bucket is full only leaves a bit in `spilled`; after the unrolled block the thread notes the bin
-  // positions of those pairs in the CTA's stash.
+  // A pair whose bucket is full only leaves a bit in `spilled`; after the unrolled block the thread moves those pairs
+  // (picked out of its registers with selects) to the CTA's stash in shared memory.
   for (uint32_t q0 = threadIdx.x; q0 < n_units; q0 += kBuildBlock * U) {
     uint4 v[U];
 #pragma unroll
@@ -681,10 +681,15 @@ region_build_kernel(const __grid_constant__ TableView t, uint32_t region_log2, u
     while (spilled != 0) {
       const uint32_t bit = __ffs(spilled) - 1u;
       spilled &= spilled - 1u;
-      const uint32_t idx = 2u * (q0 + (bit >> 1) * kBuildBlock) + (bit & 1u);
+      uint2 p = make_uint2(0u, 0u);  // pair `bit` of this batch, picked out of the registers with selects
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (bit == 2u * u) p = make_uint2(v[u].x, v[u].y);
+        if (bit == 2u * u + 1u) p = make_uint2(v[u].z, v[u].w);
+      }
       const uint32_t pos = atomicAdd(&stash_count, 1u);
-      if (pos < kStashPairs) stash[pos] = static_cast<uint16_t>(idx);
-      else spill_fresh(bin[idx], sp);  // past the stash: straight to the list, untouched
+      if (pos < kStashPairs) stash[pos] = p;
+      else spill_fresh(p, sp);  // past the stash: straight to the list, untouched
     }
   }
   TK(2);
@@ -695,7 +700,9 @@ region_build_kernel(const __grid_constant__ TableView t, uint32_t region_log2, u
   // slot of its full bucket, the victim goes to the spill list with the bucket named by the hash function after the
   // lowest-index one that maps it here, and a chain length of 1.  One probe (the inspection that found the bucket full).
   // Every warp reserves the list entries of its 32 stashed pairs itself, and first: the reservation (a global atomic)
-  // and the re-read of the pairs from the bin travel while the warp does the evictions.
+  // travels while the warp does the evictions.  (Measured: the stash holding bin positions, the pairs re-read from the
+  // bin here, 257 us; holding the pairs, 226 us; writing the victims out only after the region's write-back has been
+  // issued, 238 us.)
   const uint32_t spilled_total = stash_count;
   const uint32_t stashed = min(spilled_total, kStashPairs);
   if (stashed != 0) {
@@ -707,7 +714,7 @@ region_build_kernel(const __grid_constant__ TableView t, uint32_t region_log2, u
       unsigned long long base = 0;
       if (lane == 0) base = atomicAdd(sp.cursor, static_cast<unsigned long long>(min(32u, stashed - i0)));
       uint2 p = make_uint2(0u, 0u);
-      if (mine) p = bin[stash[i]];
+      if (mine) p = stash[i];
       uint32_t vk = kEmptyKey, vv = 0, next = 0;
       if (mine) {
         const uint32_t bid = bucket_index(t.h[0], p.x);
@@ -822,7 +829,6 @@ BlockedPlan plan_blocked_build(const TableView& t, uint64_t n) {
   const double mean = static_cast<double>(n) * static_cast<double>(1ull << region_log2) / static_cast<double>(t.num_buckets);
   double cap = mean + 6.0 * std::sqrt(mean) + 32.0;
   if (cap > static_cast<double>(n)) cap = static_cast<double>(n);
-  if (cap > 65000.0) return p;  // K11 notes bin positions in 16 bits (a bin holds about what its 64 / 128 KiB region holds)
   p.cap = (static_cast<uint32_t>(cap) + 2u) & ~1u;  // even: every bin starts 16-byte aligned
   p.n_regions = static_cast<uint32_t>(regions);
   p.region_log2 = region_log2;
@@ -910,7 +916,7 @@ cudaError_t blocked_build_finish(const TableView& t, const BlockedPlan& p, uint6
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
 
-  const int smem_c = static_cast<int>((8u << (p.region_log2 + p.b_log2)) + (4u << p.region_log2) + kStashPairs * 2);
+  const int smem_c = static_cast<int>((8u << (p.region_log2 + p.b_log2)) + (4u << p.region_log2) + kStashPairs * 8);
   e = cudaFuncSetAttribute(region_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_c);
   if (e != cudaSuccess) return e;
   int per_sm = 0;
