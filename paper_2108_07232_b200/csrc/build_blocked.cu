@@ -708,11 +708,15 @@ region_build_kernel(const __grid_constant__ TableView t, uint32_t region_log2, u
   if (stashed != 0) {
     const int lane = threadIdx.x & 31;
     uint64_t rng = xorshift_init(mix_seed(t.seed, 0x626C6B64ull + static_cast<uint64_t>(blockIdx.x) * kBuildBlock + threadIdx.x));
+    // one reservation per warp for all of its rounds, issued before any eviction: it travels while the warp works
+    uint32_t warp_entries = 0;
+    for (uint32_t i0 = threadIdx.x - lane; i0 < stashed; i0 += kBuildBlock) warp_entries += min(32u, stashed - i0);
+    unsigned long long base = 0;
+    if (lane == 0 && warp_entries != 0) base = atomicAdd(sp.cursor, static_cast<unsigned long long>(warp_entries));
+    uint32_t done = 0;  // entries of this warp's earlier rounds
     for (uint32_t i0 = threadIdx.x - lane; i0 < stashed; i0 += kBuildBlock) {  // warp-uniform
       const uint32_t i = i0 + lane;
       const bool mine = i < stashed;
-      unsigned long long base = 0;
-      if (lane == 0) base = atomicAdd(sp.cursor, static_cast<unsigned long long>(min(32u, stashed - i0)));
       uint2 p = make_uint2(0u, 0u);
       if (mine) p = stash[i];
       uint32_t vk = kEmptyKey, vv = 0, next = 0;
@@ -740,9 +744,9 @@ region_build_kernel(const __grid_constant__ TableView t, uint32_t region_log2, u
           atomicAdd(&hole_count, 1u);  // a hole (only on an uploaded store): the pair is simply placed; the list entry becomes a tombstone
         }
       }
-      base = __shfl_sync(kFullMask, base, 0);
+      const unsigned long long warp_base = __shfl_sync(kFullMask, base, 0);
       if (mine) {
-        const unsigned long long at = base + lane;
+        const unsigned long long at = warp_base + done + lane;
         if (at < sp.cap) {
           sp.pairs[at] = make_uint2(vk, vv);
           sp.start[at] = vk == kEmptyKey ? kStartTombstone : (next | 0x80000000u);
@@ -750,6 +754,7 @@ region_build_kernel(const __grid_constant__ TableView t, uint32_t region_log2, u
           spill_dropped(vk, sp);  // the victim in hand is the pair dropped, as when a chain hits its cap
         }
       }
+      done += min(32u, stashed - i0);
     }
   }
   TK(4);
