@@ -591,6 +591,7 @@ region_build_kernel(const __grid_constant__ TableView t, uint32_t region_log2, u
   uint32_t* cnt = reinterpret_cast<uint32_t*>(sm_bytes + (static_cast<size_t>(region_buckets) << (b_log2 + 3)));
   uint2* stash = reinterpret_cast<uint2*>(cnt + region_buckets);  // the pairs whose bucket was full
   __shared__ uint32_t stash_count, hole_count;
+  __shared__ unsigned long long stash_base;
   const uint32_t region = blockIdx.x;
   const uint64_t first = static_cast<uint64_t>(region) << region_log2;
   const uint32_t first32 = static_cast<uint32_t>(first);
@@ -699,62 +700,65 @@ region_build_kernel(const __grid_constant__ TableView t, uint32_t region_log2, u
   // phase 1b: the first eviction of the stashed pairs, in shared memory (table.cpp:67-81): the pair goes into a random
   // slot of its full bucket, the victim goes to the spill list with the bucket named by the hash function after the
   // lowest-index one that maps it here, and a chain length of 1.  One probe (the inspection that found the bucket full).
-  // Every warp reserves the list entries of its 32 stashed pairs itself, and first: the reservation (a global atomic)
-  // travels while the warp does the evictions.  (Measured: the stash holding bin positions, the pairs re-read from the
+  // (Measured: the stash holding bin positions, the pairs re-read from the
   // bin here, 257 us; holding the pairs, 226 us; writing the victims out only after the region's write-back has been
   // issued, 238 us.)
   const uint32_t spilled_total = stash_count;
   const uint32_t stashed = min(spilled_total, kStashPairs);
   if (stashed != 0) {
-    const int lane = threadIdx.x & 31;
+    // ONE list reservation per CTA (thousands of CTAs reserving per warp queue up on the one cursor word: the evictions
+    // then waited 7-14 k cycles for it), issued before the evictions and picked up after them
+    unsigned long long reserved = 0;
+    if (threadIdx.x == 0) reserved = atomicAdd(sp.cursor, static_cast<unsigned long long>(stashed));
     uint64_t rng = xorshift_init(mix_seed(t.seed, 0x626C6B64ull + static_cast<uint64_t>(blockIdx.x) * kBuildBlock + threadIdx.x));
-    // one reservation per warp for all of its rounds, issued before any eviction: it travels while the warp works
-    uint32_t warp_entries = 0;
-    for (uint32_t i0 = threadIdx.x - lane; i0 < stashed; i0 += kBuildBlock) warp_entries += min(32u, stashed - i0);
-    unsigned long long base = 0;
-    if (lane == 0 && warp_entries != 0) base = atomicAdd(sp.cursor, static_cast<unsigned long long>(warp_entries));
-    uint32_t done = 0;  // entries of this warp's earlier rounds
-    for (uint32_t i0 = threadIdx.x - lane; i0 < stashed; i0 += kBuildBlock) {  // warp-uniform
-      const uint32_t i = i0 + lane;
-      const bool mine = i < stashed;
-      uint2 p = make_uint2(0u, 0u);
-      if (mine) p = stash[i];
-      uint32_t vk = kEmptyKey, vv = 0, next = 0;
-      if (mine) {
+    constexpr int kRounds = (kStashPairs + kBuildBlock - 1) / kBuildBlock;
+    uint32_t vk[kRounds], vv[kRounds], nx[kRounds];
+#pragma unroll
+    for (int r = 0; r < kRounds; ++r) {
+      const uint32_t i = r * kBuildBlock + threadIdx.x;
+      vk[r] = kEmptyKey, vv[r] = 0, nx[r] = 0;
+      if (i < stashed) {
+        const uint2 p = stash[i];
         const uint32_t bid = bucket_index(t.h[0], p.x);
         const uint32_t lb = bid - first32;
         const unsigned long long old = atomicExch(rows + (lb << b_log2) + xorshift_next_below(rng, B), pack_pair(p.x, p.y));
-        vk = static_cast<uint32_t>(old);
-        vv = static_cast<uint32_t>(old >> 32);
-        if (vk != kEmptyKey) {
+        vk[r] = static_cast<uint32_t>(old);
+        vv[r] = static_cast<uint32_t>(old >> 32);
+        if (vk[r] != kEmptyKey) {
           if (fresh) {
             // every pair of a freshly built region sits in its H0 bucket, so the lowest-index hash function that maps
             // the victim here is H0 and its walk goes on at H1 (table.cpp:74-80)
-            next = bucket_index(t.h[1], vk);
+            nx[r] = bucket_index(t.h[1], vk[r]);
           } else {
             uint32_t cand[4];
 #pragma unroll
-            for (int h = 0; h < 4; ++h) cand[h] = h < static_cast<int>(t.n_hashes) ? bucket_index(t.h[h], vk) : 0u;
-            next = cand[0];
+            for (int h = 0; h < 4; ++h) cand[h] = h < static_cast<int>(t.n_hashes) ? bucket_index(t.h[h], vk[r]) : 0u;
+            uint32_t next = cand[0];
 #pragma unroll
             for (int h = 3; h >= 0; --h)  // lowest matching index wins (table.cpp:74-80)
               if (h < static_cast<int>(t.n_hashes) && cand[h] == bid) next = cand[h + 1 < static_cast<int>(t.n_hashes) ? h + 1 : 0];
+            nx[r] = next;
           }
         } else {
           atomicAdd(&hole_count, 1u);  // a hole (only on an uploaded store): the pair is simply placed; the list entry becomes a tombstone
         }
       }
-      const unsigned long long warp_base = __shfl_sync(kFullMask, base, 0);
-      if (mine) {
-        const unsigned long long at = warp_base + done + lane;
+    }
+    if (threadIdx.x == 0) stash_base = reserved;
+    __syncthreads();
+    const unsigned long long base = stash_base;
+#pragma unroll
+    for (int r = 0; r < kRounds; ++r) {
+      const uint32_t i = r * kBuildBlock + threadIdx.x;
+      if (i < stashed) {
+        const unsigned long long at = base + i;
         if (at < sp.cap) {
-          sp.pairs[at] = make_uint2(vk, vv);
-          sp.start[at] = vk == kEmptyKey ? kStartTombstone : (next | 0x80000000u);
-        } else if (vk != kEmptyKey) {
-          spill_dropped(vk, sp);  // the victim in hand is the pair dropped, as when a chain hits its cap
+          sp.pairs[at] = make_uint2(vk[r], vv[r]);
+          sp.start[at] = vk[r] == kEmptyKey ? kStartTombstone : (nx[r] | 0x80000000u);
+        } else if (vk[r] != kEmptyKey) {
+          spill_dropped(vk[r], sp);  // the victim in hand is the pair dropped, as when a chain hits its cap
         }
       }
-      done += min(32u, stashed - i0);
     }
   }
   TK(4);
