@@ -229,7 +229,8 @@ class ShardedTable:
         attempted, inserted, failed, probes = (int(x) for x in t.tolist())
         fl = [int(x) for x in fk.tolist()]
         if overflow is not None and fl[1] != 0:
-            raise RoutingOverflow("sharded insert: a routing segment overflowed; re-run with exact=True")
+            raise RoutingOverflow("sharded insert: a routing segment overflowed, its surplus pairs were not sent; "
+                                  "clear the table and re-run with exact=True")
         return BuildOutcome(inserted == attempted, inserted, failed, attempted, probes, None if fl[0] < 0 else fl[0])
 
     # -- the hot path
