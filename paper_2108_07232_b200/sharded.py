@@ -321,25 +321,35 @@ class ShardedTable:
         chunks = self._chunks(n)
         cap = self.segment_cap(self._longest_chunk)  # the same on every rank
         self.ops.overflow.zero_()
-        pending = None
+        # three stages in flight: the keys of chunk i + 1 travel while chunk i is probed and the answers of chunk i - 1 travel back
+        arriving, returning = None, None
 
-        def drain(p):
+        def probe(p):
             lo, hi, rk, wk, index = p
             wk.wait()
             answers = self.ops.find(rk)  # padding slots hold the sentinel key: answered EMPTY without a probe
             back = self.ops.empty(self.world * cap)
-            dist.all_to_all_single(back, answers, group=self.group)  # reverse route, same equal splits
+            wb = dist.all_to_all_single(back, answers, group=self.group, async_op=True)  # reverse route, same equal splits
+            return lo, hi, back, wb, index, answers
+
+        def deliver(p):
+            lo, hi, back, wb, index, _answers = p
+            wb.wait()
             self.ops.unpermute(back, index, out[lo:hi])  # padding slots carry the index 0xFFFFFFFF: skipped
 
         for lo, hi in chunks:
             sk, _, index, _counts = self.ops.partition_fixed(self.alpha, self.beta, self.world, keys[lo:hi], None, True, cap)
             rk = self.ops.empty(self.world * cap)
             wk = dist.all_to_all_single(rk, sk, group=self.group, async_op=True)
-            if pending is not None:
-                drain(pending)
-            pending = (lo, hi, rk, wk, index)
-        if pending is not None:
-            drain(pending)
+            probed = probe(arriving) if arriving is not None else None
+            if returning is not None:
+                deliver(returning)
+            arriving, returning = (lo, hi, rk, wk, index), probed
+        probed = probe(arriving) if arriving is not None else None
+        if returning is not None:
+            deliver(returning)
+        if probed is not None:
+            deliver(probed)
         flag = self.ops.overflow.to(torch.int64)
         dist.all_reduce(flag, op=dist.ReduceOp.MAX, group=self.group)
         if int(flag.item()) != 0:  # the one host read of the call
