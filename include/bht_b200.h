@@ -145,7 +145,9 @@ int32_t bht_device_of(const bht_table* table);
  * key, every pair is attempted; pairs that do not fit are reported in `result`, not as an error.
  * `result` may be NULL (no synchronisation; fetch it later with bht_last_insert_result).
  * `values` may be NULL: every key is paired with value_for_key(key) as in the reference's keys-only build
- * (table.cpp:234, keygen.hpp:23-26); the values are made on the device, so a BHT_MEM_HOST caller ships keys only. */
+ * (table.cpp:234, keygen.hpp:23-26); the values are made on the device, so a BHT_MEM_HOST caller ships keys only.
+ * A BHT_MEM_HOST call returns when the caller's arrays have been read; with result == NULL its device work may still be
+ * in flight, ordered before anything done later with this table or enqueued later on `stream`. */
 bht_status bht_insert(bht_table* table, const uint32_t* keys, const uint32_t* values, uint64_t n,
                       int32_t mem_space, bht_insert_result* result, void* stream);
 
