@@ -899,7 +899,7 @@ cudaError_t blocked_build_scatter(const TableView& t, const BlockedPlan& p, uint
   const uint32_t inv_per = static_cast<uint32_t>((1ull << 32) / p.per) + 1u;  // exact quotient for fine ids < 2^16, per <= 256
   const uint64_t tiles = (len + kSplitTile - 1) / kSplitTile;
   const int grid = static_cast<int>(std::min<uint64_t>(tiles, static_cast<uint64_t>(sm_count) * BHT_SPLIT_CTAS));
-  static const cudaError_t attr = cudaFuncSetAttribute(group_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  const cudaError_t attr = cudaFuncSetAttribute(group_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                       static_cast<int>(sizeof(SplitShared)));
   if (attr != cudaSuccess) return attr;
   const GroupArgs ga{t.h[0], p.region_log2, inv_per, p.n_groups, p.group_cap, keys, values, len, len_dev, m.group_cursor, m.grouped, sp, aligned ? 1 : 0};
@@ -916,7 +916,7 @@ cudaError_t blocked_build_finish(const TableView& t, const BlockedPlan& p, uint6
   const Spill sp{m.spill, m.spill_start, m.spill_cursor, n, log.ctr, log.failed_keys, log.failed_cap};
   const uint64_t tiles_b = static_cast<uint64_t>(p.n_groups) * ((p.group_cap + kSplitTile - 1) / kSplitTile);
   const int grid_b = static_cast<int>(std::min<uint64_t>(tiles_b, static_cast<uint64_t>(sm_count) * BHT_SPLIT_CTAS));
-  static const cudaError_t attr = cudaFuncSetAttribute(bin_split_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  const cudaError_t attr = cudaFuncSetAttribute(bin_split_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                       static_cast<int>(sizeof(SplitShared)));
   if (attr != cudaSuccess) return attr;
   const BinArgs ba{t.h[0], p.region_log2, p.per, p.n_groups, p.n_regions, p.cap, p.group_cap, m.grouped, m.group_cursor, m.bin_cursor, m.bins, sp};
@@ -950,7 +950,7 @@ cudaError_t launch_shard_split_fixed(uint32_t alpha, uint32_t beta, uint32_t n_s
   cudaError_t e = cudaMemsetAsync(cursor32, 0, sizeof(uint32_t) * n_shards, stream);
   if (e != cudaSuccess) return e;
   if (n != 0) {
-    static const cudaError_t attr = cudaFuncSetAttribute(shard_split_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    const cudaError_t attr = cudaFuncSetAttribute(shard_split_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                         static_cast<int>(sizeof(SplitShared)));
     if (attr != cudaSuccess) return attr;
     ShardSplitArgs a{};
