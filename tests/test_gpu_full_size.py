@@ -39,7 +39,9 @@ CELLS = [
 def test_full_size_properties(bht, workload, kind, b, lf, t, ref_probes):
     present, absent, values, checksum = workload
     out = torch.empty(N, dtype=torch.int32, device="cuda")
-    for attempt in range(8):  # fresh hash constants per failed build (experiments.cpp:69-82)
+    # fresh hash constants per failed build, within the reference's failure budget of 50 (experiments.cpp:62-84): the
+    # 1cht cell at load factor 0.9 builds about four times in ten at this size (profiles/r02p_paper_scale_200_builds.txt)
+    for attempt in range(40):
         cfg = bht.make_config(kind, N, lf, b, threshold=t, seed=bht.mix_seed(3, 0x100 + attempt))
         table, o = bht.build(present, cfg, values, device=0)
         if o.success:
