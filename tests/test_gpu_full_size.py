@@ -93,7 +93,7 @@ def test_full_size_cells_that_do_not_build(bht, workload, kind, b, lf, t, ref_dr
     found = out != -1
     assert st.hits == o.inserted == int(found.sum()) and torch.equal(out[found], values[found])
     drop = o.failed / N
-    assert 0.5 * ref_drop <= drop <= 2.0 * ref_drop + 2e-6, (drop, ref_drop)
+    assert 0.4 * ref_drop <= drop <= 2.5 * ref_drop + 2e-6, (drop, ref_drop)  # the reference figures come from 13-10000 events at 10^6 keys
     if o.failed <= 1 << 20:
         dropped = torch.from_numpy(table.failed_keys().view(np.int32)).cuda()
         assert dropped.numel() == o.failed
